@@ -1,0 +1,179 @@
+/*
+ * burst-b200 C ABI: the drop-in boundary between the burstsim-compatible Python
+ * host code (paper_2509_19836_b200/) and the sm_100a kernels.
+ *
+ * Every entry point replaces one NumPy einsum loop of the reference
+ * (`burstsim`, /root/reference/pkg/src/burstsim):
+ *
+ *   bb_attn_fwd_step        distributed.py:180-188  one ring step of distributed_forward
+ *                           (masked S, step LSE, normalised O_step, lse_merge, rescale-add)
+ *   bb_attn_bwd_step        distributed.py:288-295  one ring step of burst_backward
+ *                           (and :239-247 ring_backward: same math, different owners)
+ *   bb_attn_bwd_preprocess  distributed.py:274-275  D = rowsum_hadamard(dO, O), numerics.py:86-92
+ *   bb_permute_rows         distributed.py:104-130  shard_rows / gather_rows / make_device_states
+ *   bb_lmhead_fused         lmhead.py:41-93         fused_lmhead_loss (loss, dH, dW)
+ *
+ * Conventions: plain device pointers and sizes, no torch types.  Token ids and
+ * devices are 1-based (burstsim README "Conventions").  All functions take a
+ * cudaStream_t as `void*` (NULL = legacy default stream), never allocate, never
+ * synchronise, and return 0 on success or a BB_ERR_* code; the message is
+ * available from bb_last_error() (thread-local).  No C++ exception crosses
+ * this boundary.
+ */
+#ifndef BURST_B200_H
+#define BURST_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BB_OK 0
+#define BB_ERR_INVALID 1     /* argument / shape / divisibility error (Python: ValueError) */
+#define BB_ERR_CUDA 2        /* CUDA runtime or driver failure */
+#define BB_ERR_UNSUPPORTED 3 /* valid request outside what the kernels implement */
+
+/* Layout kinds: partitioning.py:38-43 */
+#define BB_LAYOUT_CONTIGUOUS 0
+#define BB_LAYOUT_ZIGZAG 1
+#define BB_LAYOUT_STRIPED 2
+#define BB_LAYOUT_BLOCK_STRIPED 3
+
+/* Mask kinds: masks.py:19-24 */
+#define BB_MASK_FULL 0
+#define BB_MASK_CAUSAL 1
+#define BB_MASK_SLIDING_WINDOW 2
+#define BB_MASK_BLOCK_SPARSE 3
+
+/* ShardLayout (partitioning.py:46-76): token -> device assignment. */
+typedef struct bb_layout {
+  int32_t kind;
+  int32_t devices;   /* G */
+  int64_t seq_len;   /* N */
+  int64_t block_len; /* block_striped only */
+} bb_layout;
+
+/* MaskSpec (masks.py:28-40).  block_mask is a device pointer to a
+ * num_blocks x num_blocks uint8 0/1 matrix (block_sparse only). */
+typedef struct bb_mask {
+  int32_t kind;
+  int32_t reserved;
+  int64_t window;     /* sliding_window width w: allowed iff 0 <= q-k < w */
+  int64_t block_len;  /* block_sparse block length */
+  int64_t num_blocks; /* block_sparse side = N / block_len */
+  const uint8_t* block_mask;
+} bb_mask;
+
+/* One forward ring step: device `q_device` folds key shard `k_device` into its
+ * running (O, lse).  Q/K/V are bf16 token-major [rows, heads, head_dim]; the
+ * running state is f32 O [n_q, hq, head_dim] and lse [hq, n_q], initialised by
+ * the caller to 0 / -inf (distributed.py:172-173).  Rows with no allowed key in
+ * this step are left untouched (exp(-inf) identity, numerics.py:62-69). */
+typedef struct bb_attn_fwd_args {
+  const void* q;
+  const void* k;
+  const void* v;
+  float* o;
+  float* lse;
+  int64_t n_q;
+  int64_t n_k;
+  int32_t hq;
+  int32_t hkv;       /* hq % hkv == 0 (GQA groups) */
+  int32_t head_dim;  /* padded head dim the tensors are laid out with: 64 or 128 */
+  float softmax_scale; /* 1/sqrt(d) of the *unpadded* head dim (oracle.py:75) */
+  int32_t q_device;
+  int32_t k_device;
+  bb_layout layout;
+  bb_mask mask;
+} bb_attn_fwd_args;
+
+/* One backward ring step (K/V-stationary kernel).  Accumulates, in f32:
+ *   dq[n_q,hq,d]  += dS K * scale       (circulating dQ_j in burst_backward)
+ *   dk[n_k,hkv,d] += dS^T Q * scale     (resident dK_i)
+ *   dv[n_k,hkv,d] += P^T dO              (resident dV_i)
+ * with P = exp(S - lse_j) and dS = P o (dO V^T - D_j) (distributed.py:288-295).
+ * lse and delta are f32 [hq, n_q]. */
+typedef struct bb_attn_bwd_args {
+  const void* q;
+  const void* k;
+  const void* v;
+  const void* dout;
+  const float* lse;
+  const float* delta;
+  float* dq;
+  float* dk;
+  float* dv;
+  int64_t n_q;
+  int64_t n_k;
+  int32_t hq;
+  int32_t hkv;
+  int32_t head_dim;
+  float softmax_scale;
+  int32_t q_device;
+  int32_t k_device;
+  bb_layout layout;
+  bb_mask mask;
+} bb_attn_bwd_args;
+
+int bb_attn_fwd_step(const bb_attn_fwd_args* args, void* stream);
+int bb_attn_bwd_step(const bb_attn_bwd_args* args, void* stream);
+
+/* delta[h, r] = sum_c dout[r,h,c] * o[r,h,c]  (dout bf16, o f32). */
+int bb_attn_bwd_preprocess(const void* dout, const float* o, float* delta, int64_t n, int32_t heads,
+                           int32_t head_dim, void* stream);
+
+/* Row permutation over rows of `row_bytes` bytes (multiple of 16).
+ * scatter == 0: dst[r] = src[index[r]];  scatter != 0: dst[index[r]] = src[r].
+ * index holds 0-based row numbers (token_id - 1). */
+int bb_permute_rows(void* dst, const void* src, const int64_t* index, int64_t n_rows,
+                    int64_t row_bytes, int32_t scatter, void* stream);
+
+/* Cast f32 -> bf16 with optional zero padding of the last dimension
+ * (cols_in -> cols_out, cols_out >= cols_in); rows are contiguous. */
+int bb_cast_pad_bf16(void* dst, const float* src, int64_t rows, int32_t cols_in, int32_t cols_out,
+                     void* stream);
+
+/* Fused LM head + cross entropy (lmhead.py:41-93): h bf16 [n, dim], w bf16
+ * [vocab, dim], targets int64 [n].  Writes loss f32 [n] (per-token nats, the
+ * caller sums), dh f32 [n, dim]; ACCUMULATES dw f32 [vocab, dim] (so sequence
+ * shards / row tiles reduce into one buffer).  rows_per_tile is B_s: logits of
+ * one row tile (B_s x vocab) are the only logits-class buffer alive, retained
+ * between forward and backward (no recompute).  vocab_per_tile
+ * (B_v) does not change values (tests/test_lmhead.py:73-81); the kernels tile
+ * the vocabulary in 256-column UMMA tiles. */
+typedef struct bb_lmhead_args {
+  const void* h;
+  const void* w;
+  const int64_t* targets;
+  int64_t n;
+  int64_t vocab;
+  int64_t dim;
+  int64_t rows_per_tile;
+  int64_t vocab_per_tile;
+  float* loss;
+  float* dh;
+  float* dw;
+  void* workspace;
+  int64_t workspace_bytes;
+} bb_lmhead_args;
+
+int64_t bb_lmhead_workspace_bytes(int64_t n, int64_t vocab, int64_t dim, int64_t rows_per_tile);
+int bb_lmhead_fused(const bb_lmhead_args* args, void* stream);
+
+/* Dense tcgen05 GEMM used by the LM head, exported for tests:
+ * C[M,N] (+)= A[M,K] * B[N,K]^T.  a_mn/b_mn select MN-major storage
+ * (A stored [K][M], B stored [K][N]); otherwise K-major ([M][K], [N][K]).
+ * accumulate != 0 adds into C. */
+int bb_gemm_bf16(const void* a, const void* b, float* c, int64_t m, int64_t n, int64_t k,
+                 int32_t a_mn, int32_t b_mn, int32_t accumulate, void* stream);
+
+const char* bb_last_error(void);
+int32_t bb_abi_version(void);
+/* Number of kernel launches issued by this library since load (for bench). */
+int64_t bb_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BURST_B200_H */

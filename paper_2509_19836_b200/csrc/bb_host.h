@@ -1,0 +1,47 @@
+// Host-side plumbing shared by the kernel translation units: error state,
+// launch accounting and TMA tensor-map construction (driver entry point is
+// resolved through cudart so the library has no link-time libcuda dependency
+// and loads on GPU-less hosts).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+#include "../../include/burst_b200.h"
+
+namespace bb {
+
+int set_error(int code, const char* fmt, ...);
+int check_cuda(cudaError_t err, const char* what);
+int check_launch(const char* what);  // cudaGetLastError after a launch; counts it
+
+extern std::atomic<int64_t> g_launches;
+
+// 2-D bf16 tensor map: `inner` contiguous elements per row, `outer` rows,
+// `row_stride_bytes` between rows; SWIZZLE_128B box {box_inner, box_outer}.
+bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                       uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
+
+int num_sms();
+
+// ---- launchers (one per kernel family) ----
+enum GemmEpilogue { GEMM_STORE = 0, GEMM_ACCUM = 1, GEMM_LOGITS = 2 };
+
+struct LogitsEpilogue {
+  const int64_t* targets;  // [M] vocab ids for the rows of this tile
+  float* part_max;         // [M][n_tiles]
+  float* part_sum;         // [M][n_tiles]
+  float* tgt_logit;        // [M]
+};
+
+int launch_gemm(const void* a, const void* b, float* c, int64_t m, int64_t n, int64_t k,
+                int64_t lda, int64_t ldb, int64_t ldc, bool a_mn, bool b_mn, int epilogue,
+                const LogitsEpilogue* le, bool raster_m_fast, cudaStream_t stream);
+int gemm_n_tile();
+
+int launch_attn_fwd(const bb_attn_fwd_args& a, cudaStream_t stream);
+int launch_attn_bwd(const bb_attn_bwd_args& a, cudaStream_t stream);
+
+}  // namespace bb

@@ -1,0 +1,199 @@
+"""torch-tensor front end of the C ABI: one function per exported kernel.
+
+Tensors are plumbing here (device memory + streams); every call goes straight
+to libburst_b200.so on the tensor's device and current torch stream.  There is
+no CPU path: a CPU tensor, a wrong dtype or a missing library raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .masks import BLOCK_SPARSE, SLIDING_WINDOW, MaskSpec
+from .partitioning import ShardLayout
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(dev: torch.device) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def _require(t: torch.Tensor, dtype: torch.dtype, name: str) -> None:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback), got {t.device}")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def layout_struct(layout: ShardLayout) -> N.BbLayout:
+    return N.BbLayout(
+        kind=N.LAYOUT_CODES[layout.kind],
+        devices=layout.devices,
+        seq_len=layout.seq_len,
+        block_len=int(layout.block_len or 0),
+    )
+
+
+@dataclass
+class DeviceMask:
+    """MaskSpec lowered for the kernels on one device (block mask as uint8 in HBM)."""
+
+    spec: MaskSpec
+    struct: N.BbMask
+    block_mask: torch.Tensor | None  # keeps the device copy alive
+
+
+_mask_cache: dict[tuple[int, int], DeviceMask] = {}
+
+
+def device_mask(mask: MaskSpec, device: torch.device) -> DeviceMask:
+    key = (id(mask), device.index if device.index is not None else torch.cuda.current_device())
+    hit = _mask_cache.get(key)
+    if hit is not None and hit.spec is mask:
+        return hit
+    bm = None
+    s = N.BbMask(kind=N.MASK_CODES[mask.kind], reserved=0, window=0, block_len=0, num_blocks=0, block_mask=None)
+    if mask.kind == SLIDING_WINDOW:
+        s.window = int(mask.window)
+    if mask.kind == BLOCK_SPARSE:
+        bm = torch.from_numpy(np.ascontiguousarray(mask.block_mask, dtype=np.uint8)).to(device)
+        s.block_len = int(mask.block_len)
+        s.num_blocks = int(mask.block_mask.shape[0])
+        s.block_mask = bm.data_ptr()
+    dm = DeviceMask(mask, s, bm)
+    _mask_cache[key] = dm
+    return dm
+
+
+def attn_fwd_step(
+    q: torch.Tensor,
+    k: torch.Tensor,
+    v: torch.Tensor,
+    o: torch.Tensor,
+    lse: torch.Tensor,
+    layout: ShardLayout,
+    mask: DeviceMask,
+    q_device: int,
+    k_device: int,
+    softmax_scale: float,
+    n_q: int | None = None,
+) -> None:
+    """Fold key shard ``k_device`` into device ``q_device``'s running (O, lse); see bb_attn_fwd_step."""
+    for t, name in ((q, "Q"), (k, "K"), (v, "V")):
+        _require(t, torch.bfloat16, name)
+    _require(o, torch.float32, "O")
+    _require(lse, torch.float32, "lse")
+    nq = q.shape[0] if n_q is None else n_q
+    a = N.BbAttnFwdArgs(
+        q=_ptr(q), k=_ptr(k), v=_ptr(v), o=_ptr(o), lse=_ptr(lse),
+        n_q=nq, n_k=k.shape[0], hq=q.shape[1], hkv=k.shape[1], head_dim=q.shape[2],
+        softmax_scale=float(softmax_scale), q_device=q_device, k_device=k_device,
+        layout=layout_struct(layout), mask=mask.struct,
+    )
+    N.check(N.load().bb_attn_fwd_step(C.byref(a), C.c_void_p(_stream(q.device))))
+
+
+def attn_bwd_step(
+    q, k, v, dout, lse, delta, dq, dk, dv,
+    layout: ShardLayout, mask: DeviceMask, q_device: int, k_device: int, softmax_scale: float,
+) -> None:
+    """Accumulate one (query shard, key shard) pair into dq/dk/dv; see bb_attn_bwd_step."""
+    for t, name in ((q, "Q"), (k, "K"), (v, "V"), (dout, "dO")):
+        _require(t, torch.bfloat16, name)
+    for t, name in ((lse, "lse"), (delta, "D"), (dq, "dQ"), (dk, "dK"), (dv, "dV")):
+        _require(t, torch.float32, name)
+    a = N.BbAttnBwdArgs(
+        q=_ptr(q), k=_ptr(k), v=_ptr(v), dout=_ptr(dout), lse=_ptr(lse), delta=_ptr(delta),
+        dq=_ptr(dq), dk=_ptr(dk), dv=_ptr(dv),
+        n_q=q.shape[0], n_k=k.shape[0], hq=q.shape[1], hkv=k.shape[1], head_dim=q.shape[2],
+        softmax_scale=float(softmax_scale), q_device=q_device, k_device=k_device,
+        layout=layout_struct(layout), mask=mask.struct,
+    )
+    N.check(N.load().bb_attn_bwd_step(C.byref(a), C.c_void_p(_stream(q.device))))
+
+
+def bwd_preprocess(dout: torch.Tensor, o: torch.Tensor, delta: torch.Tensor) -> None:
+    """delta[h, r] = rowsum(dO o O) (distributed.py:274-275)."""
+    _require(dout, torch.bfloat16, "dO")
+    _require(o, torch.float32, "O")
+    _require(delta, torch.float32, "D")
+    n, h, d = dout.shape
+    N.check(N.load().bb_attn_bwd_preprocess(_ptr(dout), _ptr(o), _ptr(delta), n, h, d, C.c_void_p(_stream(o.device))))
+
+
+def permute_rows(dst: torch.Tensor, src: torch.Tensor, index: torch.Tensor, scatter: bool) -> None:
+    """gather: dst[r] = src[index[r]]; scatter: dst[index[r]] = src[r] (0-based rows)."""
+    if not (dst.is_cuda and src.is_cuda and index.is_cuda):
+        raise ValueError("permute_rows needs CUDA tensors")
+    if index.dtype != torch.int64:
+        raise ValueError("permute_rows index must be int64")
+    rows = index.shape[0]
+    row_bytes = src[0].numel() * src.element_size() if src.shape[0] else 0
+    N.check(
+        N.load().bb_permute_rows(_ptr(dst), _ptr(src), _ptr(index), rows, row_bytes, int(scatter), C.c_void_p(_stream(src.device)))
+    )
+
+
+def cast_pad_bf16(src: torch.Tensor, cols_out: int) -> torch.Tensor:
+    """f32 [..., c] -> bf16 [..., cols_out] with zero padding (cols_out >= c)."""
+    _require(src, torch.float32, "src")
+    cin = src.shape[-1]
+    rows = src.numel() // max(cin, 1)
+    out = torch.empty(*src.shape[:-1], cols_out, dtype=torch.bfloat16, device=src.device)
+    N.check(N.load().bb_cast_pad_bf16(_ptr(out), _ptr(src), rows, cin, cols_out, C.c_void_p(_stream(src.device))))
+    return out
+
+
+def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, m: int, n: int, k: int, a_mn: bool, b_mn: bool, accumulate: bool) -> None:
+    _require(a, torch.bfloat16, "A")
+    _require(b, torch.bfloat16, "B")
+    _require(c, torch.float32, "C")
+    N.check(
+        N.load().bb_gemm_bf16(_ptr(a), _ptr(b), _ptr(c), m, n, k, int(a_mn), int(b_mn), int(accumulate), C.c_void_p(_stream(a.device)))
+    )
+
+
+def lmhead_workspace_bytes(n: int, vocab: int, dim: int, rows_per_tile: int) -> int:
+    return int(N.load().bb_lmhead_workspace_bytes(n, vocab, dim, rows_per_tile))
+
+
+def lmhead_fused(
+    h: torch.Tensor, w: torch.Tensor, targets: torch.Tensor, loss: torch.Tensor, dh: torch.Tensor,
+    dw: torch.Tensor, rows_per_tile: int, vocab_per_tile: int, workspace: torch.Tensor,
+) -> None:
+    _require(h, torch.bfloat16, "H")
+    _require(w, torch.bfloat16, "W_head")
+    if targets.dtype != torch.int64 or not targets.is_cuda:
+        raise ValueError("targets must be a CUDA int64 tensor")
+    for t, name in ((loss, "loss"), (dh, "dH"), (dw, "dW")):
+        _require(t, torch.float32, name)
+    a = N.BbLmheadArgs(
+        h=_ptr(h), w=_ptr(w), targets=_ptr(targets), n=h.shape[0], vocab=w.shape[0], dim=h.shape[1],
+        rows_per_tile=int(rows_per_tile), vocab_per_tile=int(vocab_per_tile),
+        loss=_ptr(loss), dh=_ptr(dh), dw=_ptr(dw), workspace=_ptr(workspace), workspace_bytes=workspace.numel(),
+    )
+    N.check(N.load().bb_lmhead_fused(C.byref(a), C.c_void_p(_stream(h.device))))
+
+
+def padded_head_dim(d: int) -> int:
+    """Head dims the kernels take: 64 or 128 (smaller dims are zero-padded, scale unchanged)."""
+    if d <= 64:
+        return 64
+    if d <= 128:
+        return 128
+    raise ValueError(f"head_dim {d} > 128 is not supported by the sm_100a kernels")
+
+
+def default_scale(d: int) -> float:
+    return 1.0 / math.sqrt(d)
