@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""burst-b200 benchmark: BurstAttention fwd+bwd on B200 (driver contract, one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+A step = one BurstAttention forward ring pass + one burst backward ring pass over
+the whole sequence (BASELINE.json configs[1]: LLaMA-7B attention, 32 heads,
+d=128, 128K tokens, causal, zigzag, bf16).  N=1 runs the whole sequence on one
+GPU; N>1 (torchrun, one rank per GPU, NCCL over NVLink) shards the same
+sequence over N ranks (strong scaling) through paper_2509_19836_b200.ring.
+
+value      whole-job algorithmic TFLOP/s = 14*d*H*P*K / max-over-ranks time
+           (P = exact unmasked pairs; FlashAttention convention);
+           tflops_per_gpu and mfu (vs 2250 dense bf16) are reported beside it.
+e2e        same metric through the public API with pinned HOST buffers: H2D of
+           Q/K/V/dO, fwd+bwd, D2H of dQ/dK/dV (bf16) inside the timed region.
+roofline   dominant kernel (attn_bwd) achieved FLOP/s per launch, from CUDA
+           events around its launches, vs MEASURED_PEAKS.json bf16 sustained.
+cpu_baseline  CPU oracle (oracle/burst_oracle.py, the reference algorithm) on a
+           bounded sample of the same workload, rank 0 at N=1 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+DENSE_BF16_PEAK = 2250.0  # TFLOP/s, B200 datasheet (MFU denominator)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--seq", type=int, default=131072)
+    ap.add_argument("--heads", type=int, default=32)
+    ap.add_argument("--kv-heads", type=int, default=None)
+    ap.add_argument("--head-dim", type=int, default=128)
+    ap.add_argument("--mask", default="causal", choices=["causal", "full", "window"])
+    ap.add_argument("--window", type=int, default=32768)
+    ap.add_argument("--layout", default="zigzag")
+    ap.add_argument("--backward", default="burst_backward", choices=["burst_backward", "ring_backward"])
+    ap.add_argument("--topology", default=None, help="RxM two-level ring, e.g. 2x4 (default 1xN)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def measured_peaks() -> tuple[dict, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text()), "measured"
+    return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = "index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
+            )
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out = ""
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- CPU oracle leg
+
+
+def _oracle_sample(args_tuple):
+    """One head of the reference algorithm (ring fwd + burst bwd, fp64) on a sub-sequence."""
+    n, d, g, seed = args_tuple
+    import numpy as np
+
+    from oracle import burst_oracle as O
+
+    rng = np.random.default_rng(seed)
+    q, k, v, do = (rng.uniform(-1, 1, (n, 1, d)) for _ in range(4))
+    O.mh_ring_attention(q, k, v, do, ("zigzag", n, g, None), ("causal", None, None, None), O.ring_visit(1, g), backward="burst")
+    return n * (n + 1) // 2
+
+
+def cpu_oracle_rate(d: int, cores: int, target_s: float, n: int = 2048, g: int = 4) -> dict:
+    """Time the oracle on `cores` processes (one head each) over ~target_s seconds; FLOP/s in the
+    same 14*d*P convention as the GPU number."""
+    import concurrent.futures as cf
+
+    t0 = time.perf_counter()
+    done_pairs = 0
+    heads = 0
+    with cf.ProcessPoolExecutor(max_workers=cores) as ex:
+        while True:
+            pairs = list(ex.map(_oracle_sample, [(n, d, g, 100 + heads + i) for i in range(cores)]))
+            done_pairs += sum(pairs)
+            heads += cores
+            if time.perf_counter() - t0 >= target_s:
+                break
+    dt = time.perf_counter() - t0
+    flops = 14.0 * d * done_pairs
+    return {
+        "value": flops / dt / 1e12,
+        "unit": "TFLOPS",
+        "cores": cores,
+        "seconds": round(dt, 2),
+        "sample": f"oracle (reference algorithm, fp64 NumPy einsum) ring fwd + burst bwd, zigzag causal, "
+        f"seq {n}, G={g} simulated ranks, d={d}, {heads} heads over {cores} processes",
+    }
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    """--impl reference: the reference's CPU algorithm (oracle port) on this box's host cores."""
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    # warmup + timed samples, each sample ~ one pool round
+    for _ in range(max(0, args.warmup)):
+        cpu_oracle_rate(args.head_dim, cores, 0.0)
+    t = []
+    rates = []
+    for _ in range(max(1, args.steps)):
+        r = cpu_oracle_rate(args.head_dim, cores, 0.0)
+        t.append(r["seconds"])
+        rates.append(r["value"])
+    value = statistics.median(rates)
+    line = {
+        "impl": "reference",
+        "metric": "BurstAttention fwd+bwd TFLOPS/GPU & MFU at 1M tokens, 1/2/4/8 B200",
+        "value": value,
+        "unit": "TFLOPS",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": statistics.median(t) * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (uniform [-1,1])",
+        "config": workload_config(args, world),
+        "cpu_baseline": {
+            "value": value, "unit": "TFLOPS", "cores": cores, "kind": "port",
+            "sample": r["sample"] + " (reference arm: oracle port; burstsim itself is not on the GPU box)",
+        },
+        "e2e": {"value": value, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU leg
+
+
+def workload_config(args, world: int) -> dict:
+    return {
+        "workload": f"cfg2 LLaMA-7B attention: {args.heads} heads (kv {args.kv_heads or args.heads}), d={args.head_dim}, "
+        f"seq {args.seq} {args.mask}, {args.layout} layout, fwd + {args.backward}, ring {args.topology or f'1x{world}'}",
+        "seq_len": args.seq,
+        "heads": args.heads,
+        "kv_heads": args.kv_heads or args.heads,
+        "head_dim": args.head_dim,
+        "mask": args.mask if args.mask != "window" else f"sliding_window({args.window})",
+        "layout": args.layout,
+        "backward": args.backward,
+        "parallelism": f"context-parallel ring x{world}",
+        "l2": "inputs larger than L2 (Q,K,V,dO shards >= 126 MB each at N<=8)",
+    }
+
+
+def run_gpu(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2509_19836_b200 import _native
+    from paper_2509_19836_b200 import kernels as K
+    from paper_2509_19836_b200.fabric import Topology
+    from paper_2509_19836_b200.masks import causal_mask, full_mask, sliding_window_mask, unmasked_pair_count
+    from paper_2509_19836_b200.partitioning import ShardLayout
+    from paper_2509_19836_b200.ring import ProcessRing
+
+    _native.load()
+    hq, hkv, d = args.heads, args.kv_heads or args.heads, args.head_dim
+    layout = ShardLayout(args.layout, args.seq, world)
+    mask = {"causal": causal_mask, "full": full_mask}.get(args.mask, lambda: sliding_window_mask(args.window))()
+    topo = Topology(*map(int, args.topology.split("x"))) if args.topology else None
+    ring = ProcessRing(layout, mask, topo, head_dim=d)
+    n = layout.shard_size
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+
+    def rnd(h):
+        return (torch.rand(n, h, d, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
+
+    q, k, v, do = rnd(hq), rnd(hkv), rnd(hkv), rnd(hq)
+    o = torch.empty(n, hq, d, device=dev)
+    lse = torch.empty(hq, n, device=dev)
+    dq = torch.empty(n, hq, d, device=dev)
+    dk = torch.empty(n, hkv, d, device=dev)
+    dv = torch.empty(n, hkv, d, device=dev)
+    pairs = unmasked_pair_count(mask, args.seq)
+    flops_step = 14.0 * d * hq * pairs
+    bwd_flops_step = 10.0 * d * hq * pairs
+
+    # dominant-kernel timing: CUDA events around every attn_bwd launch on the launching stream
+    bwd_events = []
+    orig_bwd = K.attn_bwd_step
+
+    def timed_bwd(*a, **kw):
+        s = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        orig_bwd(*a, **kw)
+        e1.record(s)
+        bwd_events.append((e0, e1))
+
+    import paper_2509_19836_b200.ring as ring_mod
+
+    def step():
+        ring.forward(q, k, v, o, lse)
+        ring.backward(q, k, v, do, o, lse, kind=args.backward, dq=dq, dk=dk, dv=dv)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ring_mod.K.attn_bwd_step = timed_bwd
+    ring.stats = ring_mod.RingStats()
+    launches0 = _native.launch_count()
+    stream = torch.cuda.current_stream()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+        end.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ring_mod.K.attn_bwd_step = orig_bwd
+    launches = _native.launch_count() - launches0
+    ring_bytes = ring.stats.bytes_sent // max(1, args.steps)
+    elapsed = start.elapsed_time(end) / 1e3
+    bwd_times = [a.elapsed_time(b) / 1e3 for a, b in bwd_events]
+    t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed = float(t.item())
+    value = flops_step * args.steps / elapsed / 1e12
+
+    # ---- e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        hosts = [x.cpu().pin_memory() for x in (q, k, v, do)]
+        outs = [torch.empty(n, h, d, dtype=torch.bfloat16).pin_memory() for h in (hq, hkv, hkv)]
+        dbufs = [torch.empty_like(x) for x in (q, k, v, do)]
+        h2d = sum(x.numel() * x.element_size() for x in hosts)
+        d2h = sum(x.numel() * x.element_size() for x in outs)
+
+        def e2e_step():
+            for dst, src in zip(dbufs, hosts):
+                dst.copy_(src, non_blocking=True)
+            ring.forward(dbufs[0], dbufs[1], dbufs[2], o, lse)
+            ring.backward(dbufs[0], dbufs[1], dbufs[2], dbufs[3], o, lse, kind=args.backward, dq=dq, dk=dk, dv=dv)
+            for dst, src in zip(outs, (dq, dk, dv)):
+                dst.copy_(src.to(torch.bfloat16), non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([a.elapsed_time(b) / 1e3], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {
+            "value": flops_step * args.steps / float(te.item()) / 1e12,
+            "unit": "TFLOPS",
+            "h2d_bytes_per_step": h2d * world,
+            "d2h_bytes_per_step": d2h * world,
+        }
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peaks, peak_src = measured_peaks()
+    bwd_per_launch = bwd_flops_step / max(1, len(bwd_times) // max(1, args.steps)) / world
+    avg_bwd = statistics.mean(bwd_times) if bwd_times else float("nan")
+    achieved = bwd_per_launch / avg_bwd / 1e12
+    peak = float(peaks.get("bf16_tflops_sustained", 1400.0))
+    traffic = None
+    tf = ROOT / "profiles" / "roofline_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("attn_bwd_dram_bytes_per_launch")
+    line = {
+        "metric": "BurstAttention fwd+bwd TFLOPS/GPU & MFU at 1M tokens, 1/2/4/8 B200",
+        "value": value,
+        "unit": "TFLOPS",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": elapsed / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (uniform [-1,1] bf16, torch.Generator seed 1234+rank)",
+        "config": workload_config(args, world),
+        "tflops_per_gpu": value / world,
+        "mfu": value / world / DENSE_BF16_PEAK,
+        "frac_of_measured_bf16": value / world / float(peaks.get("bf16_tflops", 1670.0)),
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "roofline": {
+            "kernel": "attn_bwd_kernel (bb_attn_bwd_step)",
+            "bound": "tensor",
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "TFLOP/s",
+            "frac": achieved / peak,
+            "traffic": traffic,
+            "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json)" if peak_src == "measured" else "fallback 1.4 PF sustained (B200_PROFILING.md)",
+            "algorithmic_flops_per_launch": bwd_per_launch,
+            "avg_launch_ms": avg_bwd * 1e3,
+            "share_of_step": sum(bwd_times) / elapsed if bwd_times else None,
+        },
+        "clocks": clk.summary(),
+        "ring_bytes_sent_per_step_rank0": ring_bytes,
+    }
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_oracle_rate(args.head_dim, 1, args.cpu_seconds)
+        line["cpu_baseline"]["kind"] = "port"
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    run_gpu(parse())
