@@ -169,6 +169,9 @@ int bb_gemm_bf16(const void* a, const void* b, float* c, int64_t m, int64_t n, i
                  int32_t a_mn, int32_t b_mn, int32_t accumulate, void* stream);
 
 const char* bb_last_error(void);
+/* Diagnostics: with BB_PROBE=1 in the environment, kernels record per-phase
+ * clock64() stamps of CTA (0,0) for its first tiles; copies n int64 to host. */
+int bb_debug_probe(int64_t* host_out, int32_t n);
 int32_t bb_abi_version(void);
 /* Number of kernel launches issued by this library since load (for bench). */
 int64_t bb_launch_count(void);

@@ -12,7 +12,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libburst_b200.so"
+LIB_PATH = Path(os.environ.get("BB_LIB_PATH") or Path(__file__).resolve().parent / "_lib" / "libburst_b200.so")
 
 BB_OK, BB_ERR_INVALID, BB_ERR_CUDA, BB_ERR_UNSUPPORTED = 0, 1, 2, 3
 
@@ -30,6 +30,7 @@ EXPORTS = (
     "bb_lmhead_fused",
     "bb_gemm_bf16",
     "bb_last_error",
+    "bb_debug_probe",
     "bb_abi_version",
     "bb_launch_count",
 )
@@ -138,6 +139,7 @@ def load(path: os.PathLike | str | None = None) -> C.CDLL:
     lib.bb_lmhead_fused.argtypes = [C.POINTER(BbLmheadArgs), vp]
     lib.bb_gemm_bf16.argtypes = [vp, vp, vp, i64, i64, i64, i32, i32, i32, vp]
     lib.bb_last_error.restype = C.c_char_p
+    lib.bb_debug_probe.argtypes = [vp, i32]
     lib.bb_abi_version.restype = i32
     lib.bb_launch_count.restype = i64
     for name in EXPORTS:

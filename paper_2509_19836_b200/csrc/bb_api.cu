@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "bb_host.h"
@@ -49,6 +50,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                        uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
+  return make_tmap_2d(map, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, inner, outer, row_stride_bytes, box_inner,
+                      box_outer);
+}
+
+bool make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype, uint64_t inner, uint64_t outer,
+                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
   auto fn = encode_fn();
   if (!fn) {
     set_error(BB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
@@ -63,7 +70,7 @@ bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner, uint6
   cuuint64_t strides[1] = {row_stride_bytes};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estride[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+  CUresult r = fn(map, dtype, 2, const_cast<void*>(base), dims, strides, box,
                   estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -73,6 +80,18 @@ bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner, uint6
     return false;
   }
   return true;
+}
+
+long long* debug_probe_buffer() {
+  static long long* buf = nullptr;
+  static bool checked = false;
+  if (!checked) {
+    checked = true;
+    const char* e = getenv("BB_PROBE");
+    if (e && *e == '1' && cudaMalloc(&buf, 4096 * sizeof(long long)) == cudaSuccess)
+      cudaMemset(buf, 0, 4096 * sizeof(long long));
+  }
+  return buf;
 }
 
 int num_sms() {
@@ -118,6 +137,13 @@ using namespace bb;
 extern "C" {
 
 const char* bb_last_error(void) { return g_err; }
+
+int bb_debug_probe(int64_t* host_out, int32_t n) {
+  long long* buf = debug_probe_buffer();
+  if (!buf) return set_error(BB_ERR_UNSUPPORTED, "set BB_PROBE=1 before the first launch");
+  if (n > 4096) n = 4096;
+  return check_cuda(cudaMemcpy(host_out, buf, n * sizeof(long long), cudaMemcpyDeviceToHost), "probe copy");
+}
 int32_t bb_abi_version(void) { return 1; }
 int64_t bb_launch_count(void) { return g_launches.load(); }
 

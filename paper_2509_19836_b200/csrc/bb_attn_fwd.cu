@@ -21,6 +21,8 @@
 // per-element predicate.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "bb_host.h"
 #include "bb_mask.cuh"
 #include "bb_ptx.cuh"
@@ -30,7 +32,11 @@ namespace {
 
 constexpr int FWD_THREADS = 384;
 constexpr int KV_SLOTS = 3;
-constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units: P may reach 2^8 before O is rescaled
+constexpr float RESCALE_THRESHOLD = 8.0f;
+#ifndef BB_POLY_EVERY
+#define BB_POLY_EVERY 1000  // measured: any FMA-pipe share of exp2 was slower on B200
+#endif
+constexpr int POLY_EVERY = BB_POLY_EVERY;  // every POLY_EVERY-th P column uses ex2_poly (>8: never)  // log2 units: P may reach 2^8 before O is rescaled
 
 template <int D>
 struct FwdSmem {
@@ -50,10 +56,16 @@ struct FwdParams {
   int32_t hq, hkv;
   float scale_log2;
   int32_t q_device, k_device;
-  bb_layout layout;
-  bb_mask mask;
+  LayoutD layout;
+  MaskD mask;
   int32_t q_pairs;  // number of 256-row query blocks
+  long long* probe;  // diagnostics (BB_PROBE=1): clock64() per phase of CTA (0,0)
 };
+
+#define FWD_PROBE(idx, slot)                                                                         \
+  do {                                                                                               \
+    if (p.probe && blockIdx.x == 0 && blockIdx.y == 0 && (idx) < 16) p.probe[512 + (idx) * 32 + (slot)] = clock64(); \
+  } while (0)
 
 __device__ __forceinline__ int32_t fwd_class(const FwdParams& p, int q, int64_t m0, int64_t j) {
   const int64_t r0 = m0 + 128 * q;
@@ -123,7 +135,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         if (fwd_class(p, 0, m0, j) == TILE_SKIP && fwd_class(p, 1, m0, j) == TILE_SKIP) continue;
         for (int which = 0; which < 2; ++which, ++use) {
           const uint32_t s = use % KV_SLOTS, ph = (use / KV_SLOTS) & 1;
+          FWD_PROBE(use >> 1, 0 + which * 2);
           mbar_wait(&kv_empty[s], ph ^ 1);
+          FWD_PROBE(use >> 1, 1 + which * 2);
           mbar_expect_tx(&kv_full[s], L::TILE);
           for (int pn = 0; pn < PANELS; ++pn)
             tma_load_2d(smem + L::KV_OFF + s * L::TILE + pn * 16384, which ? &tv : &tk, &kv_full[s],
@@ -133,58 +147,92 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
+    // Order per active kv tile j (jn = next active tile):  PV0(j), S0(jn), PV1(j), S1(jn).
+    // S0(jn) only needs softmax 0 to have consumed S0(j) (it has: P0(j) is ready), so
+    // query tile 0's softmax of jn overlaps PV1(j) and S1(jn) overlaps softmax 1 -- the
+    // tensor pipe never waits on both softmax groups at once.
     constexpr uint32_t idesc_s = idesc_bf16(128, 128, false, false);
     constexpr uint32_t idesc_o = idesc_bf16(128, D, false, true);
+    uint32_t issued[2] = {0, 0};
+    auto kv_slot = [](uint32_t use) { return use % KV_SLOTS; };
+    auto kv_par = [](uint32_t use) { return (use / KV_SLOTS) & 1; };
+    auto issue_s = [&](int q, uint32_t k_base) {
+      if (elect_one()) {
+        const uint32_t q_base = smem_u32(smem + L::Q_OFF + q * L::TILE);
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
+          umma_ss(tmem + (q * 128u), sw128_desc(q_base + off, 16, 1024), sw128_desc(k_base + off, 16, 1024),
+                  idesc_s, ks > 0);
+        }
+        umma_commit(&s_full[q]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int q, uint32_t v_base) {
+      mbar_wait(&p_full[q], issued[q] & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t p_base = smem_u32(smem + L::P_OFF + q * L::PTILE);
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const uint64_t ad = sw128_desc(p_base + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024);
+          const uint64_t bd = sw128_desc(v_base + ks * 2048, 16384, 1024);
+          umma_ss(tmem + (256u + q * D), ad, bd, idesc_o, (issued[q] | ks) != 0);
+        }
+        umma_commit(&pv_done[q]);
+      }
+      __syncwarp();
+      ++issued[q];
+    };
+    auto next_active = [&](int64_t from, int32_t* c) {
+      for (int64_t jj = from; jj < n_kt; ++jj) {
+        c[0] = fwd_class(p, 0, m0, jj);
+        c[1] = fwd_class(p, 1, m0, jj);
+        if (c[0] != TILE_SKIP || c[1] != TILE_SKIP) return jj;
+      }
+      return n_kt;
+    };
     mbar_wait(q_full, 0);
-    uint32_t use = 0, issued[2] = {0, 0};
-    for (int64_t j = 0; j < n_kt; ++j) {
-      const int32_t cls[2] = {fwd_class(p, 0, m0, j), fwd_class(p, 1, m0, j)};
-      if (cls[0] == TILE_SKIP && cls[1] == TILE_SKIP) continue;
-      const uint32_t sk = use % KV_SLOTS, phk = (use / KV_SLOTS) & 1;
-      ++use;
-      const uint32_t sv = use % KV_SLOTS, phv = (use / KV_SLOTS) & 1;
-      ++use;
-      mbar_wait(&kv_full[sk], phk);
+    int32_t cls[2], cls_n[2];
+    int64_t j = next_active(0, cls);
+    if (j < n_kt) {  // prologue: S of the first active tile
+      mbar_wait(&kv_full[kv_slot(0)], kv_par(0));
       tc_fence_after();
-      const uint32_t k_base = smem_u32(smem + L::KV_OFF + sk * L::TILE);
-      for (int q = 0; q < 2; ++q) {
-        if (cls[q] == TILE_SKIP) continue;
-        if (elect_one()) {
-          const uint32_t q_base = smem_u32(smem + L::Q_OFF + q * L::TILE);
-#pragma unroll
-          for (int ks = 0; ks < D / 16; ++ks) {
-            const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
-            umma_ss(tmem + (q * 128u), sw128_desc(q_base + off, 16, 1024),
-                    sw128_desc(k_base + off, 16, 1024), idesc_s, ks > 0);
-          }
-          umma_commit(&s_full[q]);
-        }
-        __syncwarp();
-      }
-      if (elect_one()) umma_commit(&kv_empty[sk]);
+      const uint32_t k_base = smem_u32(smem + L::KV_OFF + kv_slot(0) * L::TILE);
+      for (int q = 0; q < 2; ++q)
+        if (cls[q] != TILE_SKIP) issue_s(q, k_base);
+      if (elect_one()) umma_commit(&kv_empty[kv_slot(0)]);
       __syncwarp();
-      mbar_wait(&kv_full[sv], phv);
+    }
+    for (uint32_t t = 0; j < n_kt; ++t) {
+      const int64_t jn = next_active(j + 1, cls_n);
+      const uint32_t uv = 2 * t + 1, uk = 2 * t + 2;
+      if (lane == 0) FWD_PROBE(t, 4);
+      mbar_wait(&kv_full[kv_slot(uv)], kv_par(uv));
+      if (lane == 0) FWD_PROBE(t, 5);
       tc_fence_after();
-      const uint32_t v_base = smem_u32(smem + L::KV_OFF + sv * L::TILE);
-      for (int q = 0; q < 2; ++q) {
-        if (cls[q] == TILE_SKIP) continue;
-        mbar_wait(&p_full[q], issued[q] & 1);
+      const uint32_t v_base = smem_u32(smem + L::KV_OFF + kv_slot(uv) * L::TILE);
+      const uint32_t kn_base = smem_u32(smem + L::KV_OFF + kv_slot(uk) * L::TILE);
+      if (cls[0] != TILE_SKIP) issue_pv(0, v_base);
+      if (lane == 0) FWD_PROBE(t, 7);
+      if (jn < n_kt) {
+        mbar_wait(&kv_full[kv_slot(uk)], kv_par(uk));
         tc_fence_after();
-        if (elect_one()) {
-          const uint32_t p_base = smem_u32(smem + L::P_OFF + q * L::PTILE);
-#pragma unroll
-          for (int ks = 0; ks < 8; ++ks) {
-            const uint64_t ad = sw128_desc(p_base + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024);
-            const uint64_t bd = sw128_desc(v_base + ks * 2048, 16384, 1024);
-            umma_ss(tmem + (256u + q * D), ad, bd, idesc_o, (issued[q] | ks) != 0);
-          }
-          umma_commit(&pv_done[q]);
-        }
-        __syncwarp();
-        ++issued[q];
+        if (cls_n[0] != TILE_SKIP) issue_s(0, kn_base);
       }
-      if (elect_one()) umma_commit(&kv_empty[sv]);
+      if (cls[1] != TILE_SKIP) issue_pv(1, v_base);
+      if (lane == 0) FWD_PROBE(t, 9);
+      if (jn < n_kt) {
+        if (cls_n[1] != TILE_SKIP) issue_s(1, kn_base);
+        if (elect_one()) umma_commit(&kv_empty[kv_slot(uk)]);
+        __syncwarp();
+      }
+      if (elect_one()) umma_commit(&kv_empty[kv_slot(uv)]);
       __syncwarp();
+      j = jn;
+      cls[0] = cls_n[0];
+      cls[1] = cls_n[1];
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ softmax / correction / epilogue
@@ -203,25 +251,35 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     for (int64_t j = 0; j < n_kt; ++j) {
       const int32_t cls = fwd_class(p, q, m0, j);
       if (cls == TILE_SKIP) continue;
+      if (row == 0) FWD_PROBE(t, 16 + 8 * q);
       mbar_wait(&s_full[q], t & 1);
+      if (row == 0) FWD_PROBE(t, 17 + 8 * q);
       tc_fence_after();
+      uint4 bits = make_uint4(~0u, ~0u, ~0u, ~0u);
+      if (cls == TILE_PARTIAL)
+        bits = row_mask_bits(p.layout, p.mask, q_id, row_ok, p.k_device, j * 128, p.n_k, true);
+      if (row == 0) FWD_PROBE(t, 22 + 8 * q);
       float s[128];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(tmem + t_lane + (q * 128u) + c * 32, *reinterpret_cast<float(*)[32]>(&s[c * 32]));
+      for (int c = 0; c < 4; ++c)
+        tmem_ld32(tmem + t_lane + (q * 128u) + c * 32, *reinterpret_cast<float(*)[32]>(&s[c * 32]));
       tmem_ld_wait();
       if (cls == TILE_PARTIAL) {
-        const int64_t kv0 = j * 128;
 #pragma unroll
-        for (int c = 0; c < 128; ++c) {
-          const int64_t kr = kv0 + c;
-          bool ok = row_ok && kr < p.n_k;
-          if (ok) ok = pair_allowed(p.mask, q_id, token_id(p.layout, p.k_device, kr));
-          if (!ok) s[c] = -INFINITY;
-        }
+        for (int c = 0; c < 128; ++c)
+          if (!mask_bit(bits, c)) s[c] = -INFINITY;
       }
-      float mx = -INFINITY;
+      if (row == 0) FWD_PROBE(t, 23 + 8 * q);
+      // Row max and row sum as 8-way trees (a 128-long dependent chain is ~512+ cycles).
+      float mx8[8];
 #pragma unroll
-      for (int c = 0; c < 128; ++c) mx = fmaxf(mx, s[c]);
+      for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(s[i], s[i + 8]);
+#pragma unroll
+      for (int c = 16; c < 128; c += 8)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(mx8[i], s[c + i]);
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       const float m_tile = mx * sl2;
       const bool need = m_tile > m_run + RESCALE_THRESHOLD;
       float alpha = 1.f;
@@ -230,17 +288,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         m_run = m_tile;
         l_run *= alpha;
       }
-      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-      float lsum = 0.f;
-#pragma unroll
-      for (int c = 0; c < 128; ++c) {
-        s[c] = ex2_approx(fmaf(s[c], sl2, -m_use));
-        lsum += s[c];
-      }
-      l_run += lsum;
-      // The P buffer and the O accumulator are free once the previous P.V retired.
+      const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
+      // The P buffer and the O accumulator are free once the previous P.V retired (with the
+      // MMA order PV(j-1) .. S(j) this has already happened by the time S(j) is ready).
       if (t > 0) {
         mbar_wait(&pv_done[q], (t - 1) & 1);
+        if (row == 0) FWD_PROBE(t, 18 + 8 * q);
         tc_fence_after();
         if (__any_sync(0xffffffff, need)) {
 #pragma unroll 1
@@ -255,18 +308,41 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           tmem_st_wait();
         }
       }
+      // P = 2^(S*scale*log2e - m) on MUFU.  POLY_EVERY can move a share of the columns to a
+      // cubic on the FMA pipe (never for masked tiles, whose -inf scores need MUFU's exact 0);
+      // on B200 every share tried (1/8 .. 1/2) and integer bf16 packing measured slower, so
+      // the default keeps MUFU.EX2 + F2FP.
+      float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      auto exp_pass = [&](auto masked_tag) {
+        constexpr bool MASKED = decltype(masked_tag)::value;
 #pragma unroll
-      for (int c = 0; c < 128; c += 8) {
-        uint4 v;
-        v.x = pack_bf16(s[c + 0], s[c + 1]);
-        v.y = pack_bf16(s[c + 2], s[c + 3]);
-        v.z = pack_bf16(s[c + 4], s[c + 5]);
-        v.w = pack_bf16(s[c + 6], s[c + 7]);
-        *reinterpret_cast<uint4*>(p_tile + sw128_offset(row, c, 16384)) = v;
-      }
+        for (int c = 0; c < 128; c += 8) {
+          float e[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float x = fmaf(s[c + i], sl2, neg_m);
+            e[i] = (!MASKED && (i % POLY_EVERY) == POLY_EVERY - 1) ? ex2_poly(x) : ex2_approx(x);
+            acc8[i] += e[i];
+          }
+          uint4 pk;
+          pk.x = pack_bf16(e[0], e[1]);
+          pk.y = pack_bf16(e[2], e[3]);
+          pk.z = pack_bf16(e[4], e[5]);
+          pk.w = pack_bf16(e[6], e[7]);
+          *reinterpret_cast<uint4*>(p_tile + sw128_offset(row, c, 16384)) = pk;
+        }
+      };
+      if (cls == TILE_PARTIAL)
+        exp_pass(std::true_type{});
+      else
+        exp_pass(std::false_type{});
+      l_run += ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
+      if (row == 0) FWD_PROBE(t, 20 + 8 * q);
       fence_async_smem();
+      if (row == 0) FWD_PROBE(t, 21 + 8 * q);
       tc_fence_before();
       mbar_arrive(&p_full[q]);
+      if (row == 0) FWD_PROBE(t, 19 + 8 * q);
       ++t;
     }
 
@@ -340,9 +416,10 @@ int launch_fwd_d(const bb_attn_fwd_args& a, cudaStream_t st) {
   p.scale_log2 = a.softmax_scale * 1.4426950408889634f;
   p.q_device = a.q_device;
   p.k_device = a.k_device;
-  p.layout = a.layout;
-  p.mask = a.mask;
+  p.layout = make_layoutd(a.layout);
+  p.mask = make_maskd(a.mask);
   p.q_pairs = static_cast<int32_t>((a.n_q + 255) / 256);
+  p.probe = debug_probe_buffer();
   auto kern = attn_fwd_kernel<D>;
   static uint64_t attr_done = 0;  // per device: the attribute is per-context
   int dev = 0;

@@ -24,7 +24,13 @@ extern std::atomic<int64_t> g_launches;
 bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                        uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
 
+bool make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype, uint64_t inner, uint64_t outer,
+                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
+
 int num_sms();
+
+// BB_PROBE=1 in the environment: device buffer kernels write phase timestamps into.
+long long* debug_probe_buffer();
 
 // ---- launchers (one per kernel family) ----
 enum GemmEpilogue { GEMM_STORE = 0, GEMM_ACCUM = 1, GEMM_LOGITS = 2 };

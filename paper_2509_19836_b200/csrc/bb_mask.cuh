@@ -5,6 +5,10 @@
 //   layouts  -> partitioning.py:85-112  (contiguous / zigzag / striped / block_striped)
 //   masks    -> masks.py:89-104         (full / causal / sliding_window / block_sparse)
 // Ids are 1-based global token positions, as in the reference.
+//
+// Every divisor is resolved on the host (LayoutD / MaskD): the warp roles classify
+// tiles on their critical path, and device-side int64 division (a long MUFU.RCP
+// based subroutine) was measured at several thousand cycles per tile.
 #pragma once
 #include <cstdint>
 
@@ -16,28 +20,62 @@ enum : int32_t { LAYOUT_CONTIGUOUS = 0, LAYOUT_ZIGZAG = 1, LAYOUT_STRIPED = 2, L
 enum : int32_t { MASK_FULL = 0, MASK_CAUSAL = 1, MASK_WINDOW = 2, MASK_BLOCK = 3 };
 enum : int32_t { TILE_SKIP = 0, TILE_FULL = 1, TILE_PARTIAL = 2 };
 
+struct LayoutD {
+  int32_t kind;
+  int32_t g;      // devices
+  int64_t n;      // seq_len
+  int64_t p;      // contiguous: N/G rows per device; zigzag: N/(2G) rows per half
+  int64_t bl;     // block_striped block length
+  uint32_t per;   // block_striped: tokens per device per block (bl / G)
+};
+
+struct MaskD {
+  int32_t kind;
+  uint32_t block_len;
+  int64_t window;
+  int64_t num_blocks;
+  const uint8_t* block_mask;
+};
+
+inline LayoutD make_layoutd(const bb_layout& L) {
+  LayoutD d{};
+  d.kind = L.kind;
+  d.g = L.devices;
+  d.n = L.seq_len;
+  d.p = L.kind == LAYOUT_ZIGZAG ? L.seq_len / (2 * L.devices) : L.seq_len / L.devices;
+  d.bl = L.block_len;
+  d.per = L.kind == LAYOUT_BLOCK_STRIPED ? static_cast<uint32_t>(L.block_len / L.devices) : 1u;
+  return d;
+}
+
+inline MaskD make_maskd(const bb_mask& M) {
+  MaskD d{};
+  d.kind = M.kind;
+  d.block_len = static_cast<uint32_t>(M.block_len > 0 ? M.block_len : 1);
+  d.window = M.window;
+  d.num_blocks = M.num_blocks;
+  d.block_mask = M.block_mask;
+  return d;
+}
+
 // Global 1-based id of local row `r` (0-based) on 1-based device `dev`.
-__host__ __device__ __forceinline__ int64_t token_id(const bb_layout& L, int32_t dev, int64_t r) {
-  const int64_t g = L.devices;
+__host__ __device__ __forceinline__ int64_t token_id(const LayoutD& L, int32_t dev, int64_t r) {
   switch (L.kind) {
-    case LAYOUT_ZIGZAG: {
-      const int64_t p = L.seq_len / (2 * g);
-      return r < p ? (dev - 1) * p + r + 1 : L.seq_len - dev * p + (r - p) + 1;
-    }
+    case LAYOUT_ZIGZAG:
+      return r < L.p ? (dev - 1) * L.p + r + 1 : L.n - dev * L.p + (r - L.p) + 1;
     case LAYOUT_STRIPED:
-      return dev + g * r;
+      return dev + static_cast<int64_t>(L.g) * r;
     case LAYOUT_BLOCK_STRIPED: {
-      const int64_t per = L.block_len / g;  // tokens a device owns inside one block
-      return (r / per) * L.block_len + (r % per) * g + dev;
+      const uint32_t ru = static_cast<uint32_t>(r);  // shard rows < 2^31
+      const uint32_t blk = ru / L.per;
+      return static_cast<int64_t>(blk) * L.bl + static_cast<int64_t>(ru - blk * L.per) * L.g + dev;
     }
-    default: {  // contiguous
-      const int64_t p = L.seq_len / g;
-      return (dev - 1) * p + r + 1;
-    }
+    default:  // contiguous
+      return (dev - 1) * L.p + r + 1;
   }
 }
 
-__device__ __forceinline__ bool pair_allowed(const bb_mask& M, int64_t q, int64_t k) {
+__device__ __forceinline__ bool pair_allowed(const MaskD& M, int64_t q, int64_t k) {
   switch (M.kind) {
     case MASK_CAUSAL:
       return k <= q;
@@ -45,8 +83,11 @@ __device__ __forceinline__ bool pair_allowed(const bb_mask& M, int64_t q, int64_
       const int64_t gap = q - k;
       return gap >= 0 && gap < M.window;
     }
-    case MASK_BLOCK:
-      return M.block_mask[((q - 1) / M.block_len) * M.num_blocks + (k - 1) / M.block_len] != 0;
+    case MASK_BLOCK: {
+      const uint32_t qb = static_cast<uint32_t>(q - 1) / M.block_len;
+      const uint32_t kb = static_cast<uint32_t>(k - 1) / M.block_len;
+      return M.block_mask[static_cast<int64_t>(qb) * M.num_blocks + kb] != 0;
+    }
     default:
       return true;
   }
@@ -56,9 +97,9 @@ __device__ __forceinline__ bool pair_allowed(const bb_mask& M, int64_t q, int64_
 // Shard-local ids are strictly increasing (partitioning.py:96-111), so the
 // first/last id of a run bound every id inside it.  `full_width` is false when
 // the key tile is ragged (columns past n_k must still be masked per element).
-__device__ __forceinline__ int32_t classify_tile(const bb_layout& L, const bb_mask& M, int32_t qdev,
-                                                 int64_t r0, int64_t r1, int32_t kdev, int64_t c0,
-                                                 int64_t c1, bool full_width) {
+static __device__ __forceinline__ int32_t classify_tile(const LayoutD& L, const MaskD& M, int32_t qdev, int64_t r0,
+                                                     int64_t r1, int32_t kdev, int64_t c0, int64_t c1,
+                                                     bool full_width) {
   if (r1 <= r0 || c1 <= c0) return TILE_SKIP;
   const int64_t qa = token_id(L, qdev, r0), qb = token_id(L, qdev, r1 - 1);
   const int64_t ka = token_id(L, kdev, c0), kb = token_id(L, kdev, c1 - 1);
@@ -76,13 +117,13 @@ __device__ __forceinline__ int32_t classify_tile(const bb_layout& L, const bb_ma
       if (kb <= qa && qb - ka < M.window) cls = TILE_FULL;
       break;
     case MASK_BLOCK: {
-      const int64_t qb0 = (qa - 1) / M.block_len, qb1 = (qb - 1) / M.block_len;
-      const int64_t kb0 = (ka - 1) / M.block_len, kb1 = (kb - 1) / M.block_len;
+      const uint32_t qb0 = static_cast<uint32_t>(qa - 1) / M.block_len, qb1 = static_cast<uint32_t>(qb - 1) / M.block_len;
+      const uint32_t kb0 = static_cast<uint32_t>(ka - 1) / M.block_len, kb1 = static_cast<uint32_t>(kb - 1) / M.block_len;
       if ((qb1 - qb0 + 1) * (kb1 - kb0 + 1) <= 256) {
         bool any = false, all = true;
-        for (int64_t x = qb0; x <= qb1; ++x)
-          for (int64_t y = kb0; y <= kb1; ++y) {
-            const bool on = M.block_mask[x * M.num_blocks + y] != 0;
+        for (uint32_t x = qb0; x <= qb1; ++x)
+          for (uint32_t y = kb0; y <= kb1; ++y) {
+            const bool on = M.block_mask[static_cast<int64_t>(x) * M.num_blocks + y] != 0;
             any |= on;
             all &= on;
           }
@@ -96,6 +137,37 @@ __device__ __forceinline__ int32_t classify_tile(const bb_layout& L, const bb_ma
   }
   if (cls == TILE_FULL && !full_width) cls = TILE_PARTIAL;
   return cls;
+}
+
+// 128-bit row mask of a PARTIAL tile: bit c set iff (this thread's token, the c-th token of
+// the other side's 128-run) is allowed.  fixed_is_query: the thread owns a query row and the
+// run is keys (forward); otherwise the thread owns a key and the run is queries (backward).
+// Entries past other_n (ragged shard end) are masked.
+static __device__ __noinline__ uint4 row_mask_bits(const LayoutD& L, const MaskD& M, int64_t fixed_id,
+                                                   bool fixed_ok, int32_t other_dev, int64_t other0,
+                                                   int64_t other_n, bool fixed_is_query) {
+  uint32_t w[4];
+#pragma unroll
+  for (int wd = 0; wd < 4; ++wd) {
+    uint32_t bits = 0;
+    if (fixed_ok) {
+#pragma unroll 1
+      for (int b = 0; b < 32; ++b) {
+        const int64_t r = other0 + wd * 32 + b;
+        if (r >= other_n) break;
+        const int64_t id = token_id(L, other_dev, r);
+        const bool ok = fixed_is_query ? pair_allowed(M, fixed_id, id) : pair_allowed(M, id, fixed_id);
+        bits |= static_cast<uint32_t>(ok) << b;
+      }
+    }
+    w[wd] = bits;
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__device__ __forceinline__ bool mask_bit(const uint4& b, int c) {
+  const uint32_t word = c < 32 ? b.x : c < 64 ? b.y : c < 96 ? b.z : b.w;
+  return (word >> (c & 31)) & 1u;
 }
 
 }  // namespace bb
