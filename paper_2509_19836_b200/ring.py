@@ -66,8 +66,8 @@ class ProcessRing:
             raise ValueError(f"topology has {self.topology.total_devices} devices but layout shards {layout.devices}")
         self.order = ring_schedule(self.topology, self.rank)
         self.counts = pair_count_matrix(layout, mask)  # [query dev, key dev] allowed pairs
-        self.device = torch.device("cuda", torch.cuda.current_device())
-        self.dmask = K.device_mask(mask, self.device)
+        self.device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu")
+        self.dmask = K.device_mask(mask, self.device)  # (host-side tests swap K for a CPU double)
         self.head_dim = head_dim
         self.stats = RingStats()
 

@@ -1,0 +1,31 @@
+"""Multi-GPU ring parity over NCCL (torchrun, one process per GPU): ProcessRing with the
+sm_100a kernels against the CPU oracle.  Needs >= 2 visible GPUs (gpurun --gpus 2|4);
+skipped on a single-GPU box."""
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _gpus() -> int:
+    import torch
+
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ring_over_nccl_matches_oracle(world):
+    if _gpus() < world:
+        pytest.skip(f"needs {world} GPUs, {_gpus()} visible")
+    env = dict(os.environ, PYTHONPATH=str(ROOT))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + world), str(ROOT / "tools" / "ring_check.py")]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    assert "FAIL" not in res.stdout

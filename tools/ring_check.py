@@ -1,0 +1,67 @@
+"""Multi-GPU ring parity (torchrun, NCCL): ProcessRing with the sm_100a kernels vs the CPU oracle.
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 --master-port 29511 tools/ring_check.py
+Exits non-zero on mismatch.  Used by tests/test_ring_multigpu.py when >= 2 GPUs are visible.
+"""
+
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2509_19836_b200 import masks as M  # noqa: E402
+from paper_2509_19836_b200.fabric import Topology  # noqa: E402
+from paper_2509_19836_b200.partitioning import ShardLayout, device_token_ids  # noqa: E402
+from paper_2509_19836_b200.ring import ProcessRing  # noqa: E402
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    from oracle import burst_oracle as O
+
+    failures = 0
+    n, d = 1024 * world, 128
+    cases = [("zigzag", (1, world), "causal", 4, 4, "burst_backward"), ("zigzag", (1, world), "causal", 4, 2, "ring_backward")]
+    if world == 4:
+        cases.append(("striped", (2, 2), "window", 4, 4, "burst_backward"))
+    for kind, topo, mname, hq, hkv, backward in cases:
+        layout = ShardLayout(kind, n, world)
+        mask = {"causal": M.causal_mask(), "window": M.sliding_window_mask(n // 3)}[mname]
+        mt = {"causal": ("causal", None, None, None), "window": ("sliding_window", n // 3, None, None)}[mname]
+        rng = np.random.default_rng(1)
+        glob = [torch.from_numpy(rng.uniform(-1, 1, (n, h, d))).float().to(torch.bfloat16) for h in (hq, hkv, hkv, hq)]
+        rows = torch.from_numpy(device_token_ids(layout, rank + 1) - 1)
+        q, k, v, do = (t[rows].contiguous().to(dev) for t in glob)
+        ring = ProcessRing(layout, mask, Topology(*topo), head_dim=d)
+        o, lse = ring.forward(q, k, v)
+        dq, dk, dv = ring.backward(q, k, v, do, o, lse, kind=backward)
+        torch.cuda.synchronize()
+        ref = O.mh_ring_attention(*(t.double().numpy() for t in glob), (kind, n, world, None), mt, O.ring_visit(*topo),
+                                  backward="burst" if backward == "burst_backward" else "ring")
+        r = rows.numpy()
+        rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
+        errs = {
+            "o": float(np.abs(o.double().cpu().numpy() - ref["o"][r]).max()),
+            "lse": float(np.abs(lse.double().cpu().numpy() - ref["lse"][:, r]).max()),
+            "dq": rel(dq.double().cpu().numpy(), ref["dq"][r]),
+            "dk": rel(dk.double().cpu().numpy(), ref["dk"][r]),
+            "dv": rel(dv.double().cpu().numpy(), ref["dv"][r]),
+        }
+        ok = errs["o"] < 1e-2 and errs["lse"] < 2e-3 and errs["dq"] < 1e-2 and errs["dk"] < 1e-2 and errs["dv"] < 1e-2
+        failures += not ok
+        print(f"rank {rank} {kind} {topo} {mname} {backward}: {'ok' if ok else 'FAIL'} {errs} sent={ring.stats.bytes_sent}", flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(1 if failures else 0)
+
+
+if __name__ == "__main__":
+    main()
