@@ -33,6 +33,10 @@ namespace bb {
 namespace {
 
 constexpr int BWD_THREADS = 384;
+constexpr int MAX_QT = 2048;  // query tiles per shard the class table holds (n_q <= 262144)
+#ifndef BB_DQ_RED
+#define BB_DQ_RED 0  // 1: dQ via red.global.add.v4.f32 from registers; 0: smem staging + TMA reduce-add
+#endif
 
 template <int D>
 struct BwdSmem {
@@ -45,12 +49,14 @@ struct BwdSmem {
   static constexpr uint32_t STG_OFF = DS_OFF + 128 * 128 * 2;  // 2 x [128 x 32] fp32 dQ staging
   static constexpr uint32_t VEC_OFF = STG_OFF + 2 * 16384;     // [2][lse2 128 | delta 128]
   static constexpr uint32_t BAR_OFF = VEC_OFF + 2 * 256 * 4;
-  static constexpr uint32_t BYTES = BAR_OFF + 256;
+  static constexpr uint32_t CLS_OFF = BAR_OFF + 256;  // 2-bit tile class per query tile
+  static constexpr uint32_t BYTES = CLS_OFF + MAX_QT / 4;
 };
 
 struct BwdParams {
   const float* lse;
   const float* delta;
+  float* dq;
   float* dk;
   float* dv;
   int64_t n_q, n_k;
@@ -129,6 +135,17 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
+  // Classify this key tile against every query tile once (2 bits each); the warp roles then
+  // look classes up instead of re-deriving them per tile (that inlined id arithmetic put
+  // several KB of code on every role's per-tile path and stalled on instruction fetch).
+  uint8_t* cls_tab = smem + L::CLS_OFF;
+  for (uint32_t b = threadIdx.x; b < (n_qt + 3) / 4; b += BWD_THREADS) {
+    uint32_t byte = 0;
+    for (uint32_t k = 0; k < 4; ++k)
+      if (4 * b + k < n_qt) byte |= static_cast<uint32_t>(bwd_class(p, 4 * b + k, c0)) << (2 * k);
+    cls_tab[b] = static_cast<uint8_t>(byte);
+  }
+  auto tile_cls = [&](uint32_t qt) { return static_cast<int32_t>((cls_tab[qt >> 2] >> ((qt & 3) * 2)) & 3); };
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -146,7 +163,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       for (int64_t w = 0; w < n_work; ++w) {
         const int64_t qt = static_cast<uint32_t>(w) % n_qt;
         const int h = kv_head * group + static_cast<int>(static_cast<uint32_t>(w) / n_qt);
-        if (bwd_class(p, qt, c0) == TILE_SKIP) continue;
+        if (tile_cls(static_cast<uint32_t>(qt)) == TILE_SKIP) continue;
         const uint32_t qs = it & 1;
         BB_PROBE(0);
         mbar_wait(&q_empty[qs], ((it >> 1) & 1) ^ 1);
@@ -174,7 +191,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     uint32_t it = 0;
     for (int64_t w = 0; w < n_work; ++w) {
       const int64_t qt = static_cast<uint32_t>(w) % n_qt;
-      if (bwd_class(p, qt, c0) == TILE_SKIP) continue;
+      if (tile_cls(static_cast<uint32_t>(qt)) == TILE_SKIP) continue;
       const uint32_t qs = it & 1;
       const uint32_t q_base = smem_u32(smem + L::Q_OFF + qs * L::TILE);
       if (lane == 0) BB_PROBE(4);
@@ -254,7 +271,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 
     auto next_work = [&](int64_t from) {
       for (int64_t w = from; w < n_work; ++w)
-        if (bwd_class(p, static_cast<uint32_t>(w) % n_qt, c0) != TILE_SKIP) return w;
+        if (tile_cls(static_cast<uint32_t>(w) % n_qt) != TILE_SKIP) return w;
       return n_work;
     };
     // Raw global value only: the transform is applied at the smem store so the load's
@@ -277,9 +294,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     named_bar_sync(3, 256);
     uint32_t it = 0;
     while (w < n_work) {
+      if (ct == 0) BB_PROBE(24);
       const int64_t qt = static_cast<uint32_t>(w) % n_qt;
       const int h = kv_head * group + static_cast<int>(static_cast<uint32_t>(w) / n_qt);
-      const int32_t cls = bwd_class(p, qt, c0);
+      const int32_t cls = tile_cls(static_cast<uint32_t>(qt));
       const int64_t r0 = qt * 128;
       const int64_t w_next = next_work(w + 1);
       const float v_next = w_next < n_work ? load_vec(w_next) : 0.f;  // prefetch under this tile
@@ -317,7 +335,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       mbar_arrive(p_full);
       if (ct == 0) BB_PROBE(18);
 
-      // ---- dS^T = P^T o (dP^T - D[q]) -> smem (K-major rows = keys)
+      // ---- dS^T = P^T o (dP^T - D[q]) -> smem (K-major rows = keys).  The previous tile's
+      // dQ reduce (group 1's issuer) staged in this buffer, which both groups now overwrite:
+      // wait for the reads, then a barrier across both groups.
+      if (issuer) bulk_wait_read<0>();
+      named_bar_sync(3, 256);
       mbar_wait(dp_full, it & 1);
       if (ct == 0) BB_PROBE(19);
       tc_fence_after();
@@ -350,27 +372,55 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       mbar_wait(dq_full, it & 1);
       if (ct == 0) BB_PROBE(21);
       tc_fence_after();
+#if BB_DQ_RED
+      {  // fire-and-forget 16-byte vector reductions straight from registers (no staging)
+        const int64_t qr = r0 + row;
+        float* dst = p.dq + (qr * p.hq + h) * static_cast<int64_t>(D);
 #pragma unroll 1
-      for (int c2 = 0; c2 < D / 64; ++c2) {
-        const int dcol = g * (D / 2) + c2 * 32;
-        float v[32];
-        tmem_ld32(tmem + t_lane + COL_DP + dcol, v);
-        tmem_ld_wait();
-        if (issuer) bulk_wait_read<0>();  // previous reduce has finished reading the staging tile
-        named_bar_sync(1 + g, 128);
+        for (int c2 = 0; c2 < D / 64; ++c2) {
+          const int dcol = g * (D / 2) + c2 * 32;
+          float v[32];
+          tmem_ld32(tmem + t_lane + COL_DP + dcol, v);
+          tmem_ld_wait();
+          if (qr < p.n_q) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float4 x = make_float4(v[4 * i] * p.scale, v[4 * i + 1] * p.scale, v[4 * i + 2] * p.scale,
-                                       v[4 * i + 3] * p.scale);
-          *reinterpret_cast<float4*>(stg + row * 128 + ((i ^ (row & 7)) << 4)) = x;
+            for (int i = 0; i < 8; ++i)
+              atomicAdd(reinterpret_cast<float4*>(dst + dcol + 4 * i),
+                        make_float4(v[4 * i] * p.scale, v[4 * i + 1] * p.scale, v[4 * i + 2] * p.scale,
+                                    v[4 * i + 3] * p.scale));
+          }
+        }
+      }
+#else
+      // All of this group's dQ chunks are staged at once -- group 0 in the staging buffer,
+      // group 1 in the dS^T buffer (free: dq_full implies the dK / dQ MMAs that read dS^T
+      // retired) -- then one fence, one barrier and the TMA reduces.  The reads of the
+      // staging are waited for lazily, before the next tile's dS^T writes.
+      {
+        uint8_t* stage = g == 0 ? smem + L::STG_OFF : smem + L::DS_OFF;
+#pragma unroll
+        for (int c2 = 0; c2 < D / 64; ++c2) {
+          const int dcol = g * (D / 2) + c2 * 32;
+          float v[32];
+          tmem_ld32(tmem + t_lane + COL_DP + dcol, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 x = make_float4(v[4 * i] * p.scale, v[4 * i + 1] * p.scale, v[4 * i + 2] * p.scale,
+                                         v[4 * i + 3] * p.scale);
+            *reinterpret_cast<float4*>(stage + c2 * 16384 + row * 128 + ((i ^ (row & 7)) << 4)) = x;
+          }
         }
         fence_async_smem();
         named_bar_sync(1 + g, 128);
         if (issuer) {
-          tma_reduce_add_2d(&tdq, stg, h * D + dcol, static_cast<int32_t>(r0));
+#pragma unroll
+          for (int c2 = 0; c2 < D / 64; ++c2)
+            tma_reduce_add_2d(&tdq, stage + c2 * 16384, h * D + g * (D / 2) + c2 * 32, static_cast<int32_t>(r0));
           bulk_commit();
         }
       }
+#endif
       tc_fence_before();
       mbar_arrive(dq_free);
       if (ct == 0) BB_PROBE(22);
@@ -424,6 +474,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 
 template <int D>
 int launch_bwd_d(const bb_attn_bwd_args& a, cudaStream_t st) {
+  if ((a.n_q + 127) / 128 > MAX_QT)
+    return set_error(BB_ERR_UNSUPPORTED, "attn_bwd: query shard of %lld rows exceeds %d (raise MAX_QT)", (long long)a.n_q, MAX_QT * 128);
   CUtensorMap tq, tk, tv, tdo, tdq;
   const uint64_t qrow = static_cast<uint64_t>(a.hq) * D * 2, krow = static_cast<uint64_t>(a.hkv) * D * 2;
   if (!make_tmap_bf16_2d(&tq, a.q, static_cast<uint64_t>(a.hq) * D, a.n_q, qrow, 64, 128) ||
@@ -435,6 +487,7 @@ int launch_bwd_d(const bb_attn_bwd_args& a, cudaStream_t st) {
   BwdParams p{};
   p.lse = a.lse;
   p.delta = a.delta;
+  p.dq = a.dq;
   p.dk = a.dk;
   p.dv = a.dv;
   p.n_q = a.n_q;

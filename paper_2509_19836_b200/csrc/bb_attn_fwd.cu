@@ -31,6 +31,7 @@ namespace bb {
 namespace {
 
 constexpr int FWD_THREADS = 384;
+constexpr int MAX_KT = 2048;  // key tiles per shard the class table holds (n_k <= 262144)
 constexpr int KV_SLOTS = 3;
 constexpr float RESCALE_THRESHOLD = 8.0f;
 #ifndef BB_POLY_EVERY
@@ -46,7 +47,8 @@ struct FwdSmem {
   static constexpr uint32_t P_OFF = Q_OFF + 2 * TILE;
   static constexpr uint32_t KV_OFF = P_OFF + 2 * PTILE;
   static constexpr uint32_t BAR_OFF = KV_OFF + KV_SLOTS * TILE;
-  static constexpr uint32_t BYTES = BAR_OFF + 256;
+  static constexpr uint32_t CLS_OFF = BAR_OFF + 256;  // per key tile: class(q tile 0) | class(q tile 1) << 2
+  static constexpr uint32_t BYTES = CLS_OFF + MAX_KT;
 };
 
 struct FwdParams {
@@ -116,6 +118,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
+  // Classify both query tiles against every key tile once; the warp roles look classes up
+  // (re-deriving them per tile put the id arithmetic on every role's critical path).
+  uint8_t* cls_tab = smem + L::CLS_OFF;
+  for (int64_t jj = threadIdx.x; jj < n_kt; jj += FWD_THREADS)
+    cls_tab[jj] = static_cast<uint8_t>(fwd_class(p, 0, m0, jj) | (fwd_class(p, 1, m0, jj) << 2));
+  auto tile_cls = [&](int q, int64_t jj) { return static_cast<int32_t>((cls_tab[jj] >> (2 * q)) & 3); };
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -132,7 +140,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
                       static_cast<int32_t>(m0 + 128 * q));
       uint32_t use = 0;
       for (int64_t j = 0; j < n_kt; ++j) {
-        if (fwd_class(p, 0, m0, j) == TILE_SKIP && fwd_class(p, 1, m0, j) == TILE_SKIP) continue;
+        if (cls_tab[j] == 0) continue;  // both query tiles skip
         for (int which = 0; which < 2; ++which, ++use) {
           const uint32_t s = use % KV_SLOTS, ph = (use / KV_SLOTS) & 1;
           FWD_PROBE(use >> 1, 0 + which * 2);
@@ -187,8 +195,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     };
     auto next_active = [&](int64_t from, int32_t* c) {
       for (int64_t jj = from; jj < n_kt; ++jj) {
-        c[0] = fwd_class(p, 0, m0, jj);
-        c[1] = fwd_class(p, 1, m0, jj);
+        c[0] = tile_cls(0, jj);
+        c[1] = tile_cls(1, jj);
         if (c[0] != TILE_SKIP || c[1] != TILE_SKIP) return jj;
       }
       return n_kt;
@@ -249,7 +257,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     float m_run = -INFINITY, l_run = 0.f;
     uint32_t t = 0;
     for (int64_t j = 0; j < n_kt; ++j) {
-      const int32_t cls = fwd_class(p, q, m0, j);
+      const int32_t cls = tile_cls(q, j);
       if (cls == TILE_SKIP) continue;
       if (row == 0) FWD_PROBE(t, 16 + 8 * q);
       mbar_wait(&s_full[q], t & 1);
@@ -400,6 +408,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 
 template <int D>
 int launch_fwd_d(const bb_attn_fwd_args& a, cudaStream_t st) {
+  if ((a.n_k + 127) / 128 > MAX_KT)
+    return set_error(BB_ERR_UNSUPPORTED, "attn_fwd: key shard of %lld rows exceeds %d (raise MAX_KT)", (long long)a.n_k, MAX_KT * 128);
   CUtensorMap tq, tk, tv;
   const uint64_t qrow = static_cast<uint64_t>(a.hq) * D * 2, krow = static_cast<uint64_t>(a.hkv) * D * 2;
   if (!make_tmap_bf16_2d(&tq, a.q, static_cast<uint64_t>(a.hq) * D, a.n_q, qrow, 64, 128) ||

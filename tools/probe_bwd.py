@@ -11,7 +11,7 @@ buf = np.zeros(4096, dtype=np.int64)
 N.check(N.load().bb_debug_probe(buf.ctypes.data, 4096))
 t = buf.reshape(128, 32)[:16]
 base = t[t > 0].min()
-names = {0: "ld:q_empty?", 1: "ld:q_empty ok", 2: "ld:do_empty ok", 4: "mma:start", 5: "mma:q_full", 6: "mma:S issued", 7: "mma:dq_free", 8: "mma:p_full", 9: "mma:ds_full",
+names = {24: "c:top", 0: "ld:q_empty?", 1: "ld:q_empty ok", 2: "ld:do_empty ok", 4: "mma:start", 5: "mma:q_full", 6: "mma:S issued", 7: "mma:dq_free", 8: "mma:p_full", 9: "mma:ds_full",
          16: "c:start", 17: "c:s_full", 18: "c:P done", 19: "c:dp_full", 20: "c:dS done", 21: "c:dq_full", 22: "c:dq drained", 23: "c:end"}
 for it in range(16):
     row = " ".join(f"{names[s]}={t[it, s]-base}" for s in sorted(names) if t[it, s] > 0)
