@@ -20,8 +20,9 @@
 //   warps 4-11  two groups of 4 warps, each owning half of the 128 query columns
 //               (group g: TMEM columns of its half, all 128 lanes):
 //               P^T -> TMEM (bf16, in place over S^T), dS^T -> SWIZZLE_128B smem,
-//               dQ tile -> swizzled smem staging -> TMA bulk reduce-add (fp32) into
-//               the circulating dQ, final dK / dV read-modify-write.
+//               final dK / dV read-modify-write.
+//   warps 12-15 dQ drain: dQ tile -> swizzled smem staging -> TMA bulk reduce-add (fp32)
+//               into the circulating dQ, overlapped with the next tile's P / dS.
 // TMEM: S^T / P^T [0,128), dP^T then dQ [128,256), dV [256,256+D), dK [256+D,256+2D).
 #include <cuda_runtime.h>
 
@@ -32,7 +33,7 @@
 namespace bb {
 namespace {
 
-constexpr int BWD_THREADS = 384;
+constexpr int BWD_THREADS = 512;
 constexpr int MAX_QT = 2048;  // query tiles per shard the class table holds (n_q <= 262144)
 #ifndef BB_DQ_RED
 #define BB_DQ_RED 0  // 1: dQ via red.global.add.v4.f32 from registers; 0: smem staging + TMA reduce-add
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     mbar_init(dp_full, 1);
     mbar_init(ds_full, 256);
     mbar_init(dq_full, 1);
-    mbar_init(dq_free, 256);
+    mbar_init(dq_free, 128);
     mbar_init(acc_full, 1);
     fence_barrier_init();
   }
@@ -151,6 +152,15 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // Work items: (query head of the GQA group, query tile) in order, skipping masked tiles.
+  auto next_active = [&](int64_t from) {
+    for (int64_t w = from; w < n_work; ++w)
+      if (tile_cls(static_cast<uint32_t>(w) % n_qt) != TILE_SKIP) return w;
+    return n_work;
+  };
+  auto item_qt = [&](int64_t w) { return static_cast<uint32_t>(w) % n_qt; };
+  auto item_head = [&](int64_t w) { return kv_head * group + static_cast<int>(static_cast<uint32_t>(w) / n_qt); };
+
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
     if (elect_one()) {
@@ -160,44 +170,36 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         tma_load_2d(smem + L::V_OFF + pn * 16384, &tv, kv_full, kv_head * D + pn * 64, static_cast<int32_t>(c0));
       }
       uint32_t it = 0;
-      for (int64_t w = 0; w < n_work; ++w) {
-        const int64_t qt = static_cast<uint32_t>(w) % n_qt;
-        const int h = kv_head * group + static_cast<int>(static_cast<uint32_t>(w) / n_qt);
-        if (tile_cls(static_cast<uint32_t>(qt)) == TILE_SKIP) continue;
+      for (int64_t w = next_active(0); w < n_work; w = next_active(w + 1), ++it) {
+        const int32_t qrow0 = static_cast<int32_t>(item_qt(w) * 128);
+        const int h = item_head(w);
         const uint32_t qs = it & 1;
         BB_PROBE(0);
         mbar_wait(&q_empty[qs], ((it >> 1) & 1) ^ 1);
         BB_PROBE(1);
         mbar_expect_tx(&q_full[qs], L::TILE);
         for (int pn = 0; pn < PANELS; ++pn)
-          tma_load_2d(smem + L::Q_OFF + qs * L::TILE + pn * 16384, &tq, &q_full[qs], h * D + pn * 64,
-                      static_cast<int32_t>(qt * 128));
+          tma_load_2d(smem + L::Q_OFF + qs * L::TILE + pn * 16384, &tq, &q_full[qs], h * D + pn * 64, qrow0);
         mbar_wait(do_empty, (it & 1) ^ 1);
         BB_PROBE(2);
         mbar_expect_tx(do_full, L::TILE);
         for (int pn = 0; pn < PANELS; ++pn)
-          tma_load_2d(smem + L::DO_OFF + pn * 16384, &tdo, do_full, h * D + pn * 64, static_cast<int32_t>(qt * 128));
-        ++it;
+          tma_load_2d(smem + L::DO_OFF + pn * 16384, &tdo, do_full, h * D + pn * 64, qrow0);
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
+    // Per tile t:  dV(t) [P(t) ready], S(t+1), dK(t) dQ(t) [dS(t) ready], dP(t+1) [dQ(t) drained].
+    // S(t+1) goes out as soon as dV(t) has been issued (the tensor pipe is in order, so dV(t)
+    // reads P(t) from the S columns before S(t+1) overwrites them); the compute warps then
+    // start P(t+1) while dK(t)/dQ(t) run and the drain warps empty dQ(t).
     constexpr uint32_t idesc_st = idesc_bf16(128, 128, false, false);  // S^T, dP^T
     constexpr uint32_t idesc_acc = idesc_bf16(128, D, false, true);    // dV (TS), dK: B MN-major
     constexpr uint32_t idesc_dq = idesc_bf16(128, D, true, true);      // dQ: A = dS (MN), B = K (MN)
     const uint32_t k_base = smem_u32(smem + L::K_OFF), v_base = smem_u32(smem + L::V_OFF);
     const uint32_t do_base = smem_u32(smem + L::DO_OFF), ds_base = smem_u32(smem + L::DS_OFF);
-    mbar_wait(kv_full, 0);
-    uint32_t it = 0;
-    for (int64_t w = 0; w < n_work; ++w) {
-      const int64_t qt = static_cast<uint32_t>(w) % n_qt;
-      if (tile_cls(static_cast<uint32_t>(qt)) == TILE_SKIP) continue;
-      const uint32_t qs = it & 1;
+    auto issue_s = [&](uint32_t qs) {
       const uint32_t q_base = smem_u32(smem + L::Q_OFF + qs * L::TILE);
-      if (lane == 0) BB_PROBE(4);
-      mbar_wait(&q_full[qs], (it >> 1) & 1);
-      if (lane == 0) BB_PROBE(5);
-      tc_fence_after();
       if (elect_one()) {
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
@@ -207,11 +209,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         umma_commit(s_full);
       }
       __syncwarp();
-      mbar_wait(do_full, it & 1);
-      if (lane == 0) BB_PROBE(6);
-      if (it > 0) mbar_wait(dq_free, (it - 1) & 1);  // dP^T columns held the previous dQ tile
-      if (lane == 0) BB_PROBE(7);
-      tc_fence_after();
+    };
+    auto issue_dp = [&]() {
       if (elect_one()) {
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
@@ -221,6 +220,22 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         umma_commit(dp_full);
       }
       __syncwarp();
+    };
+    mbar_wait(kv_full, 0);
+    int64_t w = next_active(0);
+    if (w < n_work) {
+      mbar_wait(&q_full[0], 0);
+      tc_fence_after();
+      issue_s(0);
+      mbar_wait(do_full, 0);
+      tc_fence_after();
+      issue_dp();
+    }
+    for (uint32_t it = 0; w < n_work; ++it) {
+      const int64_t wn = next_active(w + 1);
+      const uint32_t qs = it & 1;
+      const uint32_t q_base = smem_u32(smem + L::Q_OFF + qs * L::TILE);
+      if (lane == 0) BB_PROBE(4);
       mbar_wait(p_full, it & 1);
       if (lane == 0) BB_PROBE(8);
       tc_fence_after();
@@ -233,6 +248,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         umma_commit(do_empty);
       }
       __syncwarp();
+      if (wn < n_work) {
+        mbar_wait(&q_full[qs ^ 1], ((it + 1) >> 1) & 1);
+        tc_fence_after();
+        issue_s(qs ^ 1);
+      }
+      if (lane == 0) BB_PROBE(5);
       mbar_wait(ds_full, it & 1);
       if (lane == 0) BB_PROBE(9);
       tc_fence_after();
@@ -251,37 +272,36 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         umma_commit(dq_full);
       }
       __syncwarp();
-      ++it;
+      if (wn < n_work) {
+        mbar_wait(do_full, (it + 1) & 1);
+        if (lane == 0) BB_PROBE(6);
+        mbar_wait(dq_free, it & 1);  // dP^T columns held dQ(t)
+        if (lane == 0) BB_PROBE(7);
+        tc_fence_after();
+        issue_dp();
+      }
+      w = wn;
     }
     if (elect_one()) umma_commit(acc_full);
     __syncwarp();
-  } else if (warp >= 4) {
-    // ------------------------------------------------ P / dS / dQ / epilogue (two column groups)
-    const int g = (warp - 4) >> 2;             // column group
+  } else if (warp >= 4 && warp < 12) {
+    // ------------------------------------------------ P / dS (two column groups) + epilogue
+    const int g = (warp - 4) >> 2;             // column group: query columns [64g, 64g+64)
     const uint32_t quad = warp & 3;
-    const int row = quad * 32 + lane;          // key row (S^T, dP^T) / query row (dQ)
+    const int row = quad * 32 + lane;          // key row of S^T / dP^T
     const int ct = threadIdx.x - 128;          // 0..255
     const uint32_t t_lane = (quad * 32) << 16;
-    const bool issuer = (quad == 0 && lane == 0);
     const int64_t krow = c0 + row;
     const bool key_ok = krow < p.n_k;
     const int64_t k_id = key_ok ? token_id(p.layout, p.k_device, krow) : 0;
     uint8_t* ds_tile = smem + L::DS_OFF;
-    uint8_t* stg = smem + L::STG_OFF + g * 16384;
 
-    auto next_work = [&](int64_t from) {
-      for (int64_t w = from; w < n_work; ++w)
-        if (tile_cls(static_cast<uint32_t>(w) % n_qt) != TILE_SKIP) return w;
-      return n_work;
-    };
     // Raw global value only: the transform is applied at the smem store so the load's
     // latency hides under the tile instead of stalling the loop top.
     auto load_vec = [&](int64_t w) {  // threads 0..127: lse of query ct; 128..255: delta
-      const int64_t qt = static_cast<uint32_t>(w) % n_qt;
-      const int h = kv_head * group + static_cast<int>(static_cast<uint32_t>(w) / n_qt);
-      const int64_t r = qt * 128 + (ct & 127);
+      const int64_t r = item_qt(w) * 128 + (ct & 127);
       if (r >= p.n_q) return ct < 128 ? -INFINITY : 0.f;
-      const int64_t at = static_cast<int64_t>(h) * p.n_q + r;
+      const int64_t at = static_cast<int64_t>(item_head(w)) * p.n_q + r;
       return __ldg((ct < 128 ? p.lse : p.delta) + at);
     };
     auto vec_val = [&](float raw) {  // lse -> lse*log2e (-inf row -> +inf so P = 0); delta as is
@@ -289,22 +309,18 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       return raw == -INFINITY ? INFINITY : raw * 1.4426950408889634f;
     };
 
-    int64_t w = next_work(0);
+    int64_t w = next_active(0);
     if (w < n_work) vec_s[ct] = vec_val(load_vec(w));
     named_bar_sync(3, 256);
     uint32_t it = 0;
     while (w < n_work) {
       if (ct == 0) BB_PROBE(24);
-      const int64_t qt = static_cast<uint32_t>(w) % n_qt;
-      const int h = kv_head * group + static_cast<int>(static_cast<uint32_t>(w) / n_qt);
-      const int32_t cls = tile_cls(static_cast<uint32_t>(qt));
-      const int64_t r0 = qt * 128;
-      const int64_t w_next = next_work(w + 1);
+      const int32_t cls = tile_cls(item_qt(w));
+      const int64_t r0 = static_cast<int64_t>(item_qt(w)) * 128;
+      const int64_t w_next = next_active(w + 1);
       const float v_next = w_next < n_work ? load_vec(w_next) : 0.f;  // prefetch under this tile
       const float* lse2 = vec_s + (it & 1) * 256;
       const float* dlt = lse2 + 128;
-
-      // ---- P^T = exp2(S^T * scale*log2e - lse2[q]) -> TMEM (bf16 pairs, over S^T)
       uint4 bits = make_uint4(~0u, ~0u, ~0u, ~0u);
       if (cls == TILE_PARTIAL) bits = row_mask_bits(p.layout, p.mask, k_id, key_ok, p.q_device, r0, p.n_q, false);
       else if (!key_ok) bits = make_uint4(0u, 0u, 0u, 0u);
@@ -312,7 +328,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       mbar_wait(s_full, it & 1);
       if (ct == 0) BB_PROBE(17);
       tc_fence_after();
-      float pr[64];
+
+      // ---- P^T = exp2(S^T * scale*log2e - lse2[q]) -> TMEM (bf16 pairs, over S^T); kept packed
+      uint32_t pk[2][16];
 #pragma unroll
       for (int c2 = 0; c2 < 2; ++c2) {
         const int c = g * 2 + c2;
@@ -320,26 +338,22 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         tmem_ld32(tmem + t_lane + COL_S + c * 32, s);
         tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
+        for (int i = 0; i < 32; i += 2) {
           const int qc = c * 32 + i;
-          const float e = ex2_approx(fmaf(s[i], p.scale_log2, -lse2[qc]));
-          pr[c2 * 32 + i] = mask_bit(bits, qc) ? e : 0.f;
+          const float e0 = ex2_approx(fmaf(s[i], p.scale_log2, -lse2[qc]));
+          const float e1 = ex2_approx(fmaf(s[i + 1], p.scale_log2, -lse2[qc + 1]));
+          pk[c2][i / 2] = pack_bf16(mask_bit(bits, qc) ? e0 : 0.f, mask_bit(bits, qc + 1) ? e1 : 0.f);
         }
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(pr[c2 * 32 + 2 * i], pr[c2 * 32 + 2 * i + 1]);
-        tmem_st16(tmem + t_lane + COL_S + g * 64 + c2 * 16, pk);
+        tmem_st16(tmem + t_lane + COL_S + g * 64 + c2 * 16, pk[c2]);
       }
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(p_full);
       if (ct == 0) BB_PROBE(18);
 
-      // ---- dS^T = P^T o (dP^T - D[q]) -> smem (K-major rows = keys).  The previous tile's
-      // dQ reduce (group 1's issuer) staged in this buffer, which both groups now overwrite:
-      // wait for the reads, then a barrier across both groups.
-      if (issuer) bulk_wait_read<0>();
-      named_bar_sync(3, 256);
+      // ---- dS^T = P^T o (dP^T - D[q]) -> smem (K-major rows = keys); the dK/dQ MMAs of the
+      // previous tile must have finished reading the buffer (dq_full(t-1)).
+      if (it > 0) mbar_wait(dq_full, (it - 1) & 1);
       mbar_wait(dp_full, it & 1);
       if (ct == 0) BB_PROBE(19);
       tc_fence_after();
@@ -356,9 +370,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int a = i + 2 * e;
-            const float b = pr[c2 * 32 + a] * (dp[a] - dlt[c * 32 + a]);
-            const float b2 = pr[c2 * 32 + a + 1] * (dp[a + 1] - dlt[c * 32 + a + 1]);
-            vw[e] = pack_bf16(b, b2);
+            const __nv_bfloat162 pb = *reinterpret_cast<const __nv_bfloat162*>(&pk[c2][a / 2]);
+            vw[e] = pack_bf16(__low2float(pb) * (dp[a] - dlt[c * 32 + a]),
+                              __high2float(pb) * (dp[a + 1] - dlt[c * 32 + a + 1]));
           }
           *reinterpret_cast<uint4*>(ds_tile + sw128_offset(row, c * 32 + i, 16384)) = v;
         }
@@ -368,70 +382,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       mbar_arrive(ds_full);
       if (ct == 0) BB_PROBE(20);
 
-      // ---- dQ tile (TMEM lane = query row) -> staging -> TMA reduce-add into dQ (fp32)
-      mbar_wait(dq_full, it & 1);
-      if (ct == 0) BB_PROBE(21);
-      tc_fence_after();
-#if BB_DQ_RED
-      {  // fire-and-forget 16-byte vector reductions straight from registers (no staging)
-        const int64_t qr = r0 + row;
-        float* dst = p.dq + (qr * p.hq + h) * static_cast<int64_t>(D);
-#pragma unroll 1
-        for (int c2 = 0; c2 < D / 64; ++c2) {
-          const int dcol = g * (D / 2) + c2 * 32;
-          float v[32];
-          tmem_ld32(tmem + t_lane + COL_DP + dcol, v);
-          tmem_ld_wait();
-          if (qr < p.n_q) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              atomicAdd(reinterpret_cast<float4*>(dst + dcol + 4 * i),
-                        make_float4(v[4 * i] * p.scale, v[4 * i + 1] * p.scale, v[4 * i + 2] * p.scale,
-                                    v[4 * i + 3] * p.scale));
-          }
-        }
-      }
-#else
-      // All of this group's dQ chunks are staged at once -- group 0 in the staging buffer,
-      // group 1 in the dS^T buffer (free: dq_full implies the dK / dQ MMAs that read dS^T
-      // retired) -- then one fence, one barrier and the TMA reduces.  The reads of the
-      // staging are waited for lazily, before the next tile's dS^T writes.
-      {
-        uint8_t* stage = g == 0 ? smem + L::STG_OFF : smem + L::DS_OFF;
-#pragma unroll
-        for (int c2 = 0; c2 < D / 64; ++c2) {
-          const int dcol = g * (D / 2) + c2 * 32;
-          float v[32];
-          tmem_ld32(tmem + t_lane + COL_DP + dcol, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 x = make_float4(v[4 * i] * p.scale, v[4 * i + 1] * p.scale, v[4 * i + 2] * p.scale,
-                                         v[4 * i + 3] * p.scale);
-            *reinterpret_cast<float4*>(stage + c2 * 16384 + row * 128 + ((i ^ (row & 7)) << 4)) = x;
-          }
-        }
-        fence_async_smem();
-        named_bar_sync(1 + g, 128);
-        if (issuer) {
-#pragma unroll
-          for (int c2 = 0; c2 < D / 64; ++c2)
-            tma_reduce_add_2d(&tdq, stage + c2 * 16384, h * D + g * (D / 2) + c2 * 32, static_cast<int32_t>(r0));
-          bulk_commit();
-        }
-      }
-#endif
-      tc_fence_before();
-      mbar_arrive(dq_free);
-      if (ct == 0) BB_PROBE(22);
-
       if (w_next < n_work) vec_s[((it + 1) & 1) * 256 + ct] = vec_val(v_next);
       named_bar_sync(3, 256);
       if (ct == 0) BB_PROBE(23);
       w = w_next;
       ++it;
     }
-    if (issuer) bulk_wait<0>();
     // ---- dK (scaled) and dV accumulate into the resident fp32 buffers
     if (it > 0) {
       mbar_wait(acc_full, 0);
@@ -465,6 +421,56 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         }
       }
     }
+  } else if (warp >= 12) {
+    // ------------------------------------------------ dQ drain (TMEM lane = query row)
+    // dQ(t) -> swizzled smem staging (two 32-column chunks at a time) -> TMA bulk reduce-add
+    // (fp32) into the circulating dQ; TMEM is released (dq_free) as soon as it has been read.
+    const uint32_t quad = warp & 3;
+    const int row = quad * 32 + lane;
+    const uint32_t t_lane = (quad * 32) << 16;
+    const bool issuer = (quad == 0 && lane == 0);
+    uint8_t* stg = smem + L::STG_OFF;
+    constexpr int CHUNKS = D / 32;
+    auto stage = [&](const float (&v)[32], int slot) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float4 x = make_float4(v[4 * i] * p.scale, v[4 * i + 1] * p.scale, v[4 * i + 2] * p.scale,
+                                     v[4 * i + 3] * p.scale);
+        *reinterpret_cast<float4*>(stg + slot * 16384 + row * 128 + ((i ^ (row & 7)) << 4)) = x;
+      }
+    };
+    uint32_t it = 0;
+    for (int64_t w = next_active(0); w < n_work; w = next_active(w + 1), ++it) {
+      const int32_t qrow0 = static_cast<int32_t>(item_qt(w) * 128);
+      const int hcol = item_head(w) * D;
+      mbar_wait(dq_full, it & 1);
+      if (row == 0) BB_PROBE(21);
+      tc_fence_after();
+#pragma unroll
+      for (int half = 0; half < CHUNKS / 2; ++half) {
+        float a[32], b[32];
+        tmem_ld32(tmem + t_lane + COL_DP + half * 64, a);
+        tmem_ld32(tmem + t_lane + COL_DP + half * 64 + 32, b);
+        tmem_ld_wait();
+        if (half == CHUNKS / 2 - 1) {  // all of dQ(t) read: release its TMEM columns
+          tc_fence_before();
+          mbar_arrive(dq_free);
+        }
+        if (issuer) bulk_wait_read<0>();  // previous reduce finished reading the staging
+        named_bar_sync(4, 128);
+        stage(a, 0);
+        stage(b, 1);
+        fence_async_smem();
+        named_bar_sync(4, 128);
+        if (issuer) {
+          tma_reduce_add_2d(&tdq, stg, hcol + half * 64, qrow0);
+          tma_reduce_add_2d(&tdq, stg + 16384, hcol + half * 64 + 32, qrow0);
+          bulk_commit();
+        }
+      }
+      if (row == 0) BB_PROBE(22);
+    }
+    if (issuer) bulk_wait<0>();
   }
 
   tc_fence_before();

@@ -37,6 +37,9 @@ constexpr float RESCALE_THRESHOLD = 8.0f;
 #ifndef BB_POLY_EVERY
 #define BB_POLY_EVERY 1000  // measured: any FMA-pipe share of exp2 was slower on B200
 #endif
+#ifndef BB_PACK_INT
+#define BB_PACK_INT 0
+#endif
 constexpr int POLY_EVERY = BB_POLY_EVERY;  // every POLY_EVERY-th P column uses ex2_poly (>8: never)  // log2 units: P may reach 2^8 before O is rescaled
 
 template <int D>
@@ -333,10 +336,17 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
             acc8[i] += e[i];
           }
           uint4 pk;
+#if BB_PACK_INT
+          pk.x = pack_bf16_int(e[0], e[1]);
+          pk.y = pack_bf16_int(e[2], e[3]);
+          pk.z = pack_bf16_int(e[4], e[5]);
+          pk.w = pack_bf16_int(e[6], e[7]);
+#else
           pk.x = pack_bf16(e[0], e[1]);
           pk.y = pack_bf16(e[2], e[3]);
           pk.z = pack_bf16(e[4], e[5]);
           pk.w = pack_bf16(e[6], e[7]);
+#endif
           *reinterpret_cast<uint4*>(p_tile + sw128_offset(row, c, 16384)) = pk;
         }
       };
