@@ -47,8 +47,10 @@ def parse():
     ap.add_argument("--heads", type=int, default=32)
     ap.add_argument("--kv-heads", type=int, default=None)
     ap.add_argument("--head-dim", type=int, default=128)
-    ap.add_argument("--mask", default="causal", choices=["causal", "full", "window"])
+    ap.add_argument("--mask", default="causal", choices=["causal", "full", "window", "swa_doc"])
     ap.add_argument("--window", type=int, default=32768)
+    ap.add_argument("--block-len", type=int, default=2048, help="block_striped block / swa_doc block granularity")
+    ap.add_argument("--doc-len", type=int, default=131072, help="swa_doc: document length (multiple of block-len)")
     ap.add_argument("--layout", default="zigzag")
     ap.add_argument("--backward", default="burst_backward", choices=["burst_backward", "ring_backward"])
     ap.add_argument("--topology", default=None, help="RxM two-level ring, e.g. 2x4 (default 1xN)")
@@ -197,6 +199,25 @@ def run_reference(args, rank: int, world: int) -> None:
 # --------------------------------------------------------------------------- GPU leg
 
 
+def make_mask(args):
+    """causal / full / token-level sliding window, or cfg4's block-granular sliding window AND
+    causal documents (a block_sparse mask, masks.py:100-103)."""
+    import numpy as np
+
+    from paper_2509_19836_b200.masks import block_sparse_mask, causal_mask, document_mask, full_mask, sliding_window_mask
+    from paper_2509_19836_b200.partitioning import block_mask_from_window
+
+    if args.mask == "causal":
+        return causal_mask()
+    if args.mask == "full":
+        return full_mask()
+    if args.mask == "window":
+        return sliding_window_mask(args.window)
+    band = block_mask_from_window(args.seq, args.block_len, args.window).block_mask
+    docs = document_mask([args.doc_len] * (args.seq // args.doc_len), args.block_len).block_mask
+    return block_sparse_mask(np.logical_and(band, docs).astype(np.int64), args.block_len)
+
+
 def workload_config(args, world: int) -> dict:
     return {
         "workload": f"cfg2 LLaMA-7B attention: {args.heads} heads (kv {args.kv_heads or args.heads}), d={args.head_dim}, "
@@ -205,7 +226,8 @@ def workload_config(args, world: int) -> dict:
         "heads": args.heads,
         "kv_heads": args.kv_heads or args.heads,
         "head_dim": args.head_dim,
-        "mask": args.mask if args.mask != "window" else f"sliding_window({args.window})",
+        "mask": {"window": f"sliding_window({args.window})",
+                 "swa_doc": f"block_sparse: sliding_window({args.window}) AND causal documents of {args.doc_len} (block {args.block_len})"}.get(args.mask, args.mask),
         "layout": args.layout,
         "backward": args.backward,
         "parallelism": f"context-parallel ring x{world}",
@@ -229,14 +251,14 @@ def run_gpu(args) -> None:
     from paper_2509_19836_b200 import _native
     from paper_2509_19836_b200 import kernels as K
     from paper_2509_19836_b200.fabric import Topology
-    from paper_2509_19836_b200.masks import causal_mask, full_mask, sliding_window_mask, unmasked_pair_count
+    from paper_2509_19836_b200.masks import unmasked_pair_count
     from paper_2509_19836_b200.partitioning import ShardLayout
     from paper_2509_19836_b200.ring import ProcessRing
 
     _native.load()
     hq, hkv, d = args.heads, args.kv_heads or args.heads, args.head_dim
-    layout = ShardLayout(args.layout, args.seq, world)
-    mask = {"causal": causal_mask, "full": full_mask}.get(args.mask, lambda: sliding_window_mask(args.window))()
+    layout = ShardLayout(args.layout, args.seq, world, args.block_len if args.layout == "block_striped" else None)
+    mask = make_mask(args)
     topo = Topology(*map(int, args.topology.split("x"))) if args.topology else None
     ring = ProcessRing(layout, mask, topo, head_dim=d)
     n = layout.shard_size

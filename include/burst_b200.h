@@ -55,7 +55,11 @@ typedef struct bb_layout {
 } bb_layout;
 
 /* MaskSpec (masks.py:28-40).  block_mask is a device pointer to a
- * num_blocks x num_blocks uint8 0/1 matrix (block_sparse only). */
+ * num_blocks x num_blocks uint8 0/1 matrix (block_sparse only).  row_span /
+ * col_span (optional, may be NULL) are device int32 [num_blocks][2] arrays with
+ * the first and last nonzero column of each block row / row of each block
+ * column ([-1, -1] if empty): the kernels use them to bound, per CTA, the tiles
+ * they consider instead of scanning the whole shard. */
 typedef struct bb_mask {
   int32_t kind;
   int32_t reserved;
@@ -63,6 +67,8 @@ typedef struct bb_mask {
   int64_t block_len;  /* block_sparse block length */
   int64_t num_blocks; /* block_sparse side = N / block_len */
   const uint8_t* block_mask;
+  const int32_t* row_span;
+  const int32_t* col_span;
 } bb_mask;
 
 /* One forward ring step: device `q_device` folds key shard `k_device` into its

@@ -48,6 +48,8 @@ class BbMask(C.Structure):
         ("block_len", C.c_int64),
         ("num_blocks", C.c_int64),
         ("block_mask", C.c_void_p),
+        ("row_span", C.c_void_p),
+        ("col_span", C.c_void_p),
     ]
 
 

@@ -34,7 +34,7 @@ namespace bb {
 namespace {
 
 constexpr int BWD_THREADS = 512;
-constexpr int MAX_QT = 2048;  // query tiles per shard the class table holds (n_q <= 262144)
+constexpr int MAX_QT = 4096;  // query tiles per shard the class table holds (n_q <= 524288)
 #ifndef BB_DQ_RED
 #define BB_DQ_RED 0  // 1: dQ via red.global.add.v4.f32 from registers; 0: smem staging + TMA reduce-add
 #endif
@@ -48,8 +48,8 @@ struct BwdSmem {
   static constexpr uint32_t DO_OFF = Q_OFF + 2 * TILE;
   static constexpr uint32_t DS_OFF = DO_OFF + TILE;  // dS^T, 128 keys x 128 queries bf16
   static constexpr uint32_t STG_OFF = DS_OFF + 128 * 128 * 2;  // 2 x [128 x 32] fp32 dQ staging
-  static constexpr uint32_t VEC_OFF = STG_OFF + 2 * 16384;     // [2][lse2 128 | delta 128]
-  static constexpr uint32_t BAR_OFF = VEC_OFF + 2 * 256 * 4;
+  static constexpr uint32_t VEC_OFF = STG_OFF + 2 * 16384;     // [lse2 128 | delta 128]
+  static constexpr uint32_t BAR_OFF = VEC_OFF + 256 * 4;
   static constexpr uint32_t CLS_OFF = BAR_OFF + 256;  // 2-bit tile class per query tile
   static constexpr uint32_t BYTES = CLS_OFF + MAX_QT / 4;
 };
@@ -109,8 +109,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   const int kv_head = blockIdx.y;
   const int group = p.hq / p.hkv;
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 128;  // low key tiles carry the most work
-  const uint32_t n_qt = static_cast<uint32_t>((p.n_q + 127) / 128);
-  const int64_t n_work = group * n_qt;  // (query head in group, query tile) pairs
+  // Query tiles that can touch this key tile (two binary searches, every thread), then the
+  // work items (query head of the GQA group, query tile in [q_lo, q_hi)).
+  int64_t q_lo, q_hi;
+  active_runs(p.layout, p.mask, token_id(p.layout, p.k_device, c0),
+              token_id(p.layout, p.k_device, min(c0 + 128, p.n_k) - 1), p.q_device, p.n_q, false, q_lo, q_hi);
+  const uint32_t nr = static_cast<uint32_t>(q_hi - q_lo);
+  const int64_t n_work = static_cast<int64_t>(group) * nr;
   const uint32_t warp = warp_id(), lane = lane_id();
 
   if (warp == 0 && lane == 0) {
@@ -140,13 +145,16 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   // look classes up instead of re-deriving them per tile (that inlined id arithmetic put
   // several KB of code on every role's per-tile path and stalled on instruction fetch).
   uint8_t* cls_tab = smem + L::CLS_OFF;
-  for (uint32_t b = threadIdx.x; b < (n_qt + 3) / 4; b += BWD_THREADS) {
+  for (uint32_t b = threadIdx.x; b < (nr + 3) / 4; b += BWD_THREADS) {
     uint32_t byte = 0;
     for (uint32_t k = 0; k < 4; ++k)
-      if (4 * b + k < n_qt) byte |= static_cast<uint32_t>(bwd_class(p, 4 * b + k, c0)) << (2 * k);
+      if (4 * b + k < nr) byte |= static_cast<uint32_t>(bwd_class(p, q_lo + 4 * b + k, c0)) << (2 * k);
     cls_tab[b] = static_cast<uint8_t>(byte);
   }
-  auto tile_cls = [&](uint32_t qt) { return static_cast<int32_t>((cls_tab[qt >> 2] >> ((qt & 3) * 2)) & 3); };
+  auto tile_cls = [&](uint32_t qt) {
+    const uint32_t x = qt - static_cast<uint32_t>(q_lo);
+    return static_cast<int32_t>((cls_tab[x >> 2] >> ((x & 3) * 2)) & 3);
+  };
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -155,11 +163,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   // Work items: (query head of the GQA group, query tile) in order, skipping masked tiles.
   auto next_active = [&](int64_t from) {
     for (int64_t w = from; w < n_work; ++w)
-      if (tile_cls(static_cast<uint32_t>(w) % n_qt) != TILE_SKIP) return w;
+      if (tile_cls(static_cast<uint32_t>(q_lo) + static_cast<uint32_t>(w) % nr) != TILE_SKIP) return w;
     return n_work;
   };
-  auto item_qt = [&](int64_t w) { return static_cast<uint32_t>(w) % n_qt; };
-  auto item_head = [&](int64_t w) { return kv_head * group + static_cast<int>(static_cast<uint32_t>(w) / n_qt); };
+  auto item_qt = [&](int64_t w) { return static_cast<uint32_t>(q_lo) + static_cast<uint32_t>(w) % nr; };
+  auto item_head = [&](int64_t w) { return kv_head * group + static_cast<int>(static_cast<uint32_t>(w) / nr); };
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
@@ -319,7 +327,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       const int64_t r0 = static_cast<int64_t>(item_qt(w)) * 128;
       const int64_t w_next = next_active(w + 1);
       const float v_next = w_next < n_work ? load_vec(w_next) : 0.f;  // prefetch under this tile
-      const float* lse2 = vec_s + (it & 1) * 256;
+      const float* lse2 = vec_s;
       const float* dlt = lse2 + 128;
       uint4 bits = make_uint4(~0u, ~0u, ~0u, ~0u);
       if (cls == TILE_PARTIAL) bits = row_mask_bits(p.layout, p.mask, k_id, key_ok, p.q_device, r0, p.n_q, false);
@@ -382,7 +390,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       mbar_arrive(ds_full);
       if (ct == 0) BB_PROBE(20);
 
-      if (w_next < n_work) vec_s[((it + 1) & 1) * 256 + ct] = vec_val(v_next);
+      named_bar_sync(3, 256);  // everyone is done with this tile's lse / D
+      if (w_next < n_work) vec_s[ct] = vec_val(v_next);
       named_bar_sync(3, 256);
       if (ct == 0) BB_PROBE(23);
       w = w_next;

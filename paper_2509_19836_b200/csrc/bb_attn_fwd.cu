@@ -31,7 +31,7 @@ namespace bb {
 namespace {
 
 constexpr int FWD_THREADS = 384;
-constexpr int MAX_KT = 2048;  // key tiles per shard the class table holds (n_k <= 262144)
+constexpr int MAX_KT = 4096;  // key tiles per shard the class table holds (n_k <= 524288)
 constexpr int KV_SLOTS = 3;
 constexpr float RESCALE_THRESHOLD = 8.0f;
 #ifndef BB_POLY_EVERY
@@ -51,7 +51,7 @@ struct FwdSmem {
   static constexpr uint32_t KV_OFF = P_OFF + 2 * PTILE;
   static constexpr uint32_t BAR_OFF = KV_OFF + KV_SLOTS * TILE;
   static constexpr uint32_t CLS_OFF = BAR_OFF + 256;  // per key tile: class(q tile 0) | class(q tile 1) << 2
-  static constexpr uint32_t BYTES = CLS_OFF + MAX_KT;
+  static constexpr uint32_t BYTES = CLS_OFF + MAX_KT / 2;  // 4 bits per key tile
 };
 
 struct FwdParams {
@@ -101,7 +101,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   const int head = blockIdx.y;
   const int kv_head = head / (p.hq / p.hkv);
   const int64_t m0 = static_cast<int64_t>(p.q_pairs - 1 - blockIdx.x) * 256;  // heavy rows first
-  const int64_t n_kt = (p.n_k + 127) / 128;
+  int64_t j_lo, j_hi;  // key tiles that can touch this CTA's queries (two binary searches, every thread)
+  active_runs(p.layout, p.mask, token_id(p.layout, p.q_device, m0),
+              token_id(p.layout, p.q_device, min(m0 + 256, p.n_q) - 1), p.k_device, p.n_k, true, j_lo, j_hi);
   const uint32_t warp = warp_id(), lane = lane_id();
 
   if (warp == 0 && lane == 0) {
@@ -124,9 +126,19 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   // Classify both query tiles against every key tile once; the warp roles look classes up
   // (re-deriving them per tile put the id arithmetic on every role's critical path).
   uint8_t* cls_tab = smem + L::CLS_OFF;
-  for (int64_t jj = threadIdx.x; jj < n_kt; jj += FWD_THREADS)
-    cls_tab[jj] = static_cast<uint8_t>(fwd_class(p, 0, m0, jj) | (fwd_class(p, 1, m0, jj) << 2));
-  auto tile_cls = [&](int q, int64_t jj) { return static_cast<int32_t>((cls_tab[jj] >> (2 * q)) & 3); };
+  for (int64_t b = threadIdx.x; b < (j_hi - j_lo + 1) / 2; b += FWD_THREADS) {
+    uint32_t byte = 0;
+    for (int k = 0; k < 2; ++k) {
+      const int64_t jj = j_lo + 2 * b + k;
+      if (jj < j_hi) byte |= static_cast<uint32_t>(fwd_class(p, 0, m0, jj) | (fwd_class(p, 1, m0, jj) << 2)) << (4 * k);
+    }
+    cls_tab[b] = static_cast<uint8_t>(byte);
+  }
+  auto tile_nib = [&](int64_t jj) {
+    const int64_t x = jj - j_lo;
+    return static_cast<uint32_t>(cls_tab[x >> 1] >> (4 * (x & 1))) & 15u;
+  };
+  auto tile_cls = [&](int q, int64_t jj) { return static_cast<int32_t>((tile_nib(jj) >> (2 * q)) & 3); };
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -142,8 +154,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           tma_load_2d(smem + L::Q_OFF + q * L::TILE + pn * 16384, &tq, q_full, head * D + pn * 64,
                       static_cast<int32_t>(m0 + 128 * q));
       uint32_t use = 0;
-      for (int64_t j = 0; j < n_kt; ++j) {
-        if (cls_tab[j] == 0) continue;  // both query tiles skip
+      for (int64_t j = j_lo; j < j_hi; ++j) {
+        if (tile_nib(j) == 0) continue;  // both query tiles skip
         for (int which = 0; which < 2; ++which, ++use) {
           const uint32_t s = use % KV_SLOTS, ph = (use / KV_SLOTS) & 1;
           FWD_PROBE(use >> 1, 0 + which * 2);
@@ -197,17 +209,17 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       ++issued[q];
     };
     auto next_active = [&](int64_t from, int32_t* c) {
-      for (int64_t jj = from; jj < n_kt; ++jj) {
+      for (int64_t jj = from; jj < j_hi; ++jj) {
         c[0] = tile_cls(0, jj);
         c[1] = tile_cls(1, jj);
         if (c[0] != TILE_SKIP || c[1] != TILE_SKIP) return jj;
       }
-      return n_kt;
+      return j_hi;
     };
     mbar_wait(q_full, 0);
     int32_t cls[2], cls_n[2];
-    int64_t j = next_active(0, cls);
-    if (j < n_kt) {  // prologue: S of the first active tile
+    int64_t j = next_active(j_lo, cls);
+    if (j < j_hi) {  // prologue: S of the first active tile
       mbar_wait(&kv_full[kv_slot(0)], kv_par(0));
       tc_fence_after();
       const uint32_t k_base = smem_u32(smem + L::KV_OFF + kv_slot(0) * L::TILE);
@@ -216,7 +228,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       if (elect_one()) umma_commit(&kv_empty[kv_slot(0)]);
       __syncwarp();
     }
-    for (uint32_t t = 0; j < n_kt; ++t) {
+    for (uint32_t t = 0; j < j_hi; ++t) {
       const int64_t jn = next_active(j + 1, cls_n);
       const uint32_t uv = 2 * t + 1, uk = 2 * t + 2;
       if (lane == 0) FWD_PROBE(t, 4);
@@ -227,14 +239,14 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       const uint32_t kn_base = smem_u32(smem + L::KV_OFF + kv_slot(uk) * L::TILE);
       if (cls[0] != TILE_SKIP) issue_pv(0, v_base);
       if (lane == 0) FWD_PROBE(t, 7);
-      if (jn < n_kt) {
+      if (jn < j_hi) {
         mbar_wait(&kv_full[kv_slot(uk)], kv_par(uk));
         tc_fence_after();
         if (cls_n[0] != TILE_SKIP) issue_s(0, kn_base);
       }
       if (cls[1] != TILE_SKIP) issue_pv(1, v_base);
       if (lane == 0) FWD_PROBE(t, 9);
-      if (jn < n_kt) {
+      if (jn < j_hi) {
         if (cls_n[1] != TILE_SKIP) issue_s(1, kn_base);
         if (elect_one()) umma_commit(&kv_empty[kv_slot(uk)]);
         __syncwarp();
@@ -259,7 +271,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 
     float m_run = -INFINITY, l_run = 0.f;
     uint32_t t = 0;
-    for (int64_t j = 0; j < n_kt; ++j) {
+    for (int64_t j = j_lo; j < j_hi; ++j) {
       const int32_t cls = tile_cls(q, j);
       if (cls == TILE_SKIP) continue;
       if (row == 0) FWD_PROBE(t, 16 + 8 * q);

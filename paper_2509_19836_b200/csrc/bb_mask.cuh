@@ -35,6 +35,8 @@ struct MaskD {
   int64_t window;
   int64_t num_blocks;
   const uint8_t* block_mask;
+  const int32_t* row_span;  // [num_blocks][2] first / last nonzero column per block row (or null)
+  const int32_t* col_span;  // [num_blocks][2] first / last nonzero row per block column (or null)
 };
 
 inline LayoutD make_layoutd(const bb_layout& L) {
@@ -55,6 +57,8 @@ inline MaskD make_maskd(const bb_mask& M) {
   d.window = M.window;
   d.num_blocks = M.num_blocks;
   d.block_mask = M.block_mask;
+  d.row_span = M.row_span;
+  d.col_span = M.col_span;
   return d;
 }
 
@@ -137,6 +141,68 @@ static __device__ __forceinline__ int32_t classify_tile(const LayoutD& L, const 
   }
   if (cls == TILE_FULL && !full_width) cls = TILE_PARTIAL;
   return cls;
+}
+
+// First index in [lo, hi) where a monotone (false..false true..true) predicate holds; hi if none.
+template <class F>
+__device__ __forceinline__ int64_t first_true(int64_t lo, int64_t hi, F pred) {
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (pred(mid))
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
+// Candidate range [lo, hi) of 128-runs on the "other" side that can touch a fixed run of
+// tokens with ids in [fa, fb]: everything outside is fully masked.  Ids grow with the run
+// index, so for causal / sliding-window masks the range comes from two binary searches;
+// full and block-sparse masks keep the whole range (the class table still skips blocks).
+//   fixed_is_query: the fixed run holds queries and the runs are keys (forward); else the
+//   fixed run holds keys and the runs are queries (backward).
+__device__ __forceinline__ void active_runs(const LayoutD& L, const MaskD& M, int64_t fa, int64_t fb,
+                                            int32_t dev, int64_t n_rows, bool fixed_is_query, int64_t& lo,
+                                            int64_t& hi) {
+  const int64_t n_runs = (n_rows + 127) / 128;
+  lo = 0;
+  hi = n_runs;
+  auto first_id = [&](int64_t j) { return token_id(L, dev, j * 128); };
+  auto last_id = [&](int64_t j) { return token_id(L, dev, min(j * 128 + 128, n_rows) - 1); };
+  if (M.kind == MASK_BLOCK && M.row_span && M.col_span) {
+    // union of the nonzero spans of the fixed run's block rows (columns), then the runs
+    // whose ids fall inside it
+    const int64_t b0 = static_cast<uint32_t>(fa - 1) / M.block_len, b1 = static_cast<uint32_t>(fb - 1) / M.block_len;
+    if (b1 - b0 > 64) return;
+    const int32_t* span = fixed_is_query ? M.row_span : M.col_span;
+    int64_t blo = INT64_MAX, bhi = -1;
+    for (int64_t b = b0; b <= b1; ++b) {
+      const int32_t s0 = span[2 * b], s1 = span[2 * b + 1];
+      if (s0 >= 0) {
+        blo = min(blo, static_cast<int64_t>(s0));
+        bhi = max(bhi, static_cast<int64_t>(s1));
+      }
+    }
+    if (bhi < 0) {
+      lo = hi = 0;
+      return;
+    }
+    const int64_t id_lo = blo * M.block_len + 1, id_hi = (bhi + 1) * M.block_len;
+    lo = first_true(0, n_runs, [&](int64_t j) { return last_id(j) >= id_lo; });
+    hi = first_true(lo, n_runs, [&](int64_t j) { return first_id(j) > id_hi; });
+    return;
+  }
+  if (M.kind != MASK_CAUSAL && M.kind != MASK_WINDOW) return;
+  if (fixed_is_query) {
+    // keys: live iff first key <= last query (causal), and last query - ... window lower edge
+    hi = first_true(0, n_runs, [&](int64_t j) { return first_id(j) > fb; });
+    if (M.kind == MASK_WINDOW) lo = first_true(0, hi, [&](int64_t j) { return fa - last_id(j) < M.window; });
+  } else {
+    // queries: live iff last query >= first key, and (window) first query - last key < w
+    lo = first_true(0, n_runs, [&](int64_t j) { return last_id(j) >= fa; });
+    if (M.kind == MASK_WINDOW) hi = first_true(lo, n_runs, [&](int64_t j) { return first_id(j) - fb >= M.window; });
+  }
 }
 
 // 128-bit row mask of a PARTIAL tile: bit c set iff (this thread's token, the c-th token of

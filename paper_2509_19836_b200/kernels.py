@@ -51,7 +51,8 @@ class DeviceMask:
 
     spec: MaskSpec
     struct: N.BbMask
-    block_mask: torch.Tensor | None  # keeps the device copy alive
+    block_mask: torch.Tensor | None  # keeps the device copies alive
+    spans: torch.Tensor | None = None
 
 
 _mask_cache: dict[tuple[int, int], DeviceMask] = {}
@@ -62,18 +63,30 @@ def device_mask(mask: MaskSpec, device: torch.device) -> DeviceMask:
     hit = _mask_cache.get(key)
     if hit is not None and hit.spec is mask:
         return hit
-    bm = None
+    bm = spans = None
     s = N.BbMask(kind=N.MASK_CODES[mask.kind], reserved=0, window=0, block_len=0, num_blocks=0, block_mask=None)
     if mask.kind == SLIDING_WINDOW:
         s.window = int(mask.window)
     if mask.kind == BLOCK_SPARSE:
-        bm = torch.from_numpy(np.ascontiguousarray(mask.block_mask, dtype=np.uint8)).to(device)
+        m = np.asarray(mask.block_mask) != 0
+        bm = torch.from_numpy(np.ascontiguousarray(m, dtype=np.uint8)).to(device)
         s.block_len = int(mask.block_len)
-        s.num_blocks = int(mask.block_mask.shape[0])
+        s.num_blocks = int(m.shape[0])
         s.block_mask = bm.data_ptr()
-    dm = DeviceMask(mask, s, bm)
+        spans = torch.from_numpy(np.concatenate([_spans(m), _spans(m.T)])).to(device)
+        s.row_span = spans.data_ptr()
+        s.col_span = spans.data_ptr() + m.shape[0] * 2 * 4
+    dm = DeviceMask(mask, s, bm, spans)
     _mask_cache[key] = dm
     return dm
+
+
+def _spans(m: np.ndarray) -> np.ndarray:
+    """[rows, 2] int32: first and last nonzero column per row of a 0/1 block mask, -1 if none."""
+    any_ = m.any(axis=1)
+    first = np.where(any_, m.argmax(axis=1), -1)
+    last = np.where(any_, m.shape[1] - 1 - m[:, ::-1].argmax(axis=1), -1)
+    return np.ascontiguousarray(np.stack([first, last], axis=1), dtype=np.int32)
 
 
 def attn_fwd_step(
