@@ -420,5 +420,23 @@ def run_gpu(args) -> None:
         dist.destroy_process_group()
 
 
+def _json_stdout():
+    """Route everything but the contract's JSON line away from stdout: NCCL and friends print
+    banners on fd 1 (e.g. "NCCL version ..."), so fd 1 becomes stderr and the line is
+    written to the original stdout."""
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    out = os.fdopen(saved, "w", buffering=1)
+    builtins_print = print
+
+    def emit(*a, **kw):
+        if kw.get("file") is None and a and isinstance(a[0], str) and a[0].startswith("{"):
+            kw["file"] = out
+        builtins_print(*a, **kw)
+
+    return emit
+
+
 if __name__ == "__main__":
+    print = _json_stdout()  # noqa: A001
     run_gpu(parse())
