@@ -1,0 +1,9 @@
+# ncu captures of the current kernels (after the plain command exits 0)
+export PYTHONPATH=$PWD
+R=${1:-r01b}
+CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu"
+$CMD > gpurun_out/plain_$R.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$R.csv $CMD > gpurun_out/ncu_launch_$R.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:attn_bwd -s 1 -c 1 -o gpurun_out/prof_bwd_$R -f $CMD > gpurun_out/ncu_bwd_$R.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 1 -c 1 -o gpurun_out/prof_fwd_$R -f $CMD > gpurun_out/ncu_fwd_$R.log 2>&1
+echo "exit $?" >> gpurun_out/ncu_launch_$R.log
