@@ -115,7 +115,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   active_runs(p.layout, p.mask, token_id(p.layout, p.k_device, c0),
               token_id(p.layout, p.k_device, min(c0 + 128, p.n_k) - 1), p.q_device, p.n_q, false, q_lo, q_hi);
   const uint32_t nr = static_cast<uint32_t>(q_hi - q_lo);
-  const int64_t n_work = static_cast<int64_t>(group) * nr;
+  // Work item w packs (head-in-group << 16 | query-tile index): no divisions on the roles'
+  // per-tile path (a u32 div/mod is a ~100-cycle dependent chain).  n_work = end sentinel.
+  const int64_t n_work = static_cast<int64_t>(group) << 16;
   const uint32_t warp = warp_id(), lane = lane_id();
 
   if (warp == 0 && lane == 0) {
@@ -161,13 +163,16 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
 
   // Work items: (query head of the GQA group, query tile) in order, skipping masked tiles.
-  auto next_active = [&](int64_t from) {
-    for (int64_t w = from; w < n_work; ++w)
-      if (tile_cls(static_cast<uint32_t>(q_lo) + static_cast<uint32_t>(w) % nr) != TILE_SKIP) return w;
-    return n_work;
+  auto next_active = [&](int64_t w) {
+    for (;;) {
+      if ((w & 0xFFFF) >= nr) w = ((w >> 16) + 1) << 16;
+      if (w >= n_work) return n_work;
+      if (tile_cls(static_cast<uint32_t>(q_lo) + static_cast<uint32_t>(w & 0xFFFF)) != TILE_SKIP) return w;
+      ++w;
+    }
   };
-  auto item_qt = [&](int64_t w) { return static_cast<uint32_t>(q_lo) + static_cast<uint32_t>(w) % nr; };
-  auto item_head = [&](int64_t w) { return kv_head * group + static_cast<int>(static_cast<uint32_t>(w) / nr); };
+  auto item_qt = [&](int64_t w) { return static_cast<uint32_t>(q_lo) + static_cast<uint32_t>(w & 0xFFFF); };
+  auto item_head = [&](int64_t w) { return kv_head * group + static_cast<int>(w >> 16); };
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
