@@ -33,7 +33,14 @@
 namespace bb {
 namespace {
 
-constexpr int BWD_THREADS = 512;
+#ifndef BB_BWD_NG
+#define BB_BWD_NG 2
+#endif
+constexpr int NG = BB_BWD_NG;              // compute column groups (4 warps each)
+constexpr int CPG = 128 / NG;              // query columns per group
+constexpr int CH = CPG / 32;               // 32-column chunks per group
+constexpr int NCOMP = NG * 128;            // compute threads
+constexpr int BWD_THREADS = 128 + NCOMP + 128;  // control warps + compute + dQ drain
 constexpr int MAX_QT = 4096;  // query tiles per shard the class table holds (n_q <= 524288)
 #ifndef BB_DQ_RED
 #define BB_DQ_RED 0  // 1: dQ via red.global.add.v4.f32 from registers; 0: smem staging + TMA reduce-add
@@ -134,9 +141,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     mbar_init(do_full, 1);
     mbar_init(do_empty, 1);
     mbar_init(s_full, 1);
-    mbar_init(p_full, 256);
+    mbar_init(p_full, NCOMP);
     mbar_init(dp_full, 1);
-    mbar_init(ds_full, 256);
+    mbar_init(ds_full, NCOMP);
     mbar_init(dq_full, 1);
     mbar_init(dq_free, 128);
     mbar_init(acc_full, 1);
@@ -255,7 +262,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       if (elect_one()) {
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {  // K = 128 query rows; P^T packed 2 per TMEM column
-          const uint32_t a_tmem = tmem + COL_S + (ks >> 2) * 64 + (ks & 3) * 8;
+          const uint32_t a_tmem = tmem + COL_S + (ks >> 1) * 32 + (ks & 1) * 8;  // P of q chunk c in its own S columns
           umma_ts(tmem + COL_DV, a_tmem, sw128_desc(do_base + ks * 2048, 16384, 1024), idesc_acc, (it | ks) != 0);
         }
         umma_commit(do_empty);
@@ -297,12 +304,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     }
     if (elect_one()) umma_commit(acc_full);
     __syncwarp();
-  } else if (warp >= 4 && warp < 12) {
+  } else if (warp >= 4 && warp < 4 + 4 * NG) {
     // ------------------------------------------------ P / dS (two column groups) + epilogue
-    const int g = (warp - 4) >> 2;             // column group: query columns [64g, 64g+64)
+    const int g = (warp - 4) >> 2;             // column group: query columns [CPG*g, CPG*(g+1))
     const uint32_t quad = warp & 3;
     const int row = quad * 32 + lane;          // key row of S^T / dP^T
-    const int ct = threadIdx.x - 128;          // 0..255
+    const int ct = threadIdx.x - 128;          // 0..NCOMP-1
     const uint32_t t_lane = (quad * 32) << 16;
     const int64_t krow = c0 + row;
     const bool key_ok = krow < p.n_k;
@@ -323,15 +330,15 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     };
 
     int64_t w = next_active(0);
-    if (w < n_work) vec_s[ct] = vec_val(load_vec(w));
-    named_bar_sync(3, 256);
+    if (w < n_work && ct < 256) vec_s[ct] = vec_val(load_vec(w));
+    named_bar_sync(3, NCOMP);
     uint32_t it = 0;
     while (w < n_work) {
       if (ct == 0) BB_PROBE(24);
       const int32_t cls = tile_cls(item_qt(w));
       const int64_t r0 = static_cast<int64_t>(item_qt(w)) * 128;
       const int64_t w_next = next_active(w + 1);
-      const float v_next = w_next < n_work ? load_vec(w_next) : 0.f;  // prefetch under this tile
+      const float v_next = (w_next < n_work && ct < 256) ? load_vec(w_next) : 0.f;  // prefetch under this tile
       const float* lse2 = vec_s;
       const float* dlt = lse2 + 128;
       uint4 bits = make_uint4(~0u, ~0u, ~0u, ~0u);
@@ -343,10 +350,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       tc_fence_after();
 
       // ---- P^T = exp2(S^T * scale*log2e - lse2[q]) -> TMEM (bf16 pairs, over S^T); kept packed
-      uint32_t pk[2][16];
+      uint32_t pk[CH][16];
 #pragma unroll
-      for (int c2 = 0; c2 < 2; ++c2) {
-        const int c = g * 2 + c2;
+      for (int c2 = 0; c2 < CH; ++c2) {
+        const int c = g * CH + c2;
         float s[32];
         tmem_ld32(tmem + t_lane + COL_S + c * 32, s);
         tmem_ld_wait();
@@ -357,7 +364,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           const float e1 = ex2_approx(fmaf(s[i + 1], p.scale_log2, -lse2[qc + 1]));
           pk[c2][i / 2] = pack_bf16(mask_bit(bits, qc) ? e0 : 0.f, mask_bit(bits, qc + 1) ? e1 : 0.f);
         }
-        tmem_st16(tmem + t_lane + COL_S + g * 64 + c2 * 16, pk[c2]);
+        tmem_st16(tmem + t_lane + COL_S + c * 32, pk[c2]);
       }
       tmem_st_wait();
       tc_fence_before();
@@ -371,8 +378,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       if (ct == 0) BB_PROBE(19);
       tc_fence_after();
 #pragma unroll
-      for (int c2 = 0; c2 < 2; ++c2) {
-        const int c = g * 2 + c2;
+      for (int c2 = 0; c2 < CH; ++c2) {
+        const int c = g * CH + c2;
         float dp[32];
         tmem_ld32(tmem + t_lane + COL_DP + c * 32, dp);
         tmem_ld_wait();
@@ -395,9 +402,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       mbar_arrive(ds_full);
       if (ct == 0) BB_PROBE(20);
 
-      named_bar_sync(3, 256);  // everyone is done with this tile's lse / D
-      if (w_next < n_work) vec_s[ct] = vec_val(v_next);
-      named_bar_sync(3, 256);
+      named_bar_sync(3, NCOMP);  // everyone is done with this tile's lse / D
+      if (w_next < n_work && ct < 256) vec_s[ct] = vec_val(v_next);
+      named_bar_sync(3, NCOMP);
       if (ct == 0) BB_PROBE(23);
       w = w_next;
       ++it;
@@ -409,8 +416,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       float* dk_row = p.dk + (krow * p.hkv + kv_head) * static_cast<int64_t>(D);
       float* dv_row = p.dv + (krow * p.hkv + kv_head) * static_cast<int64_t>(D);
 #pragma unroll 1
-      for (int c2 = 0; c2 < D / 64; ++c2) {
-        const int dcol = g * (D / 2) + c2 * 32;
+      for (int ce = g; ce < D / 32; ce += NG) {
+        const int dcol = ce * 32;
         float a[32], b[32];
         tmem_ld32(tmem + t_lane + COL_DK + dcol, a);
         tmem_ld32(tmem + t_lane + COL_DV + dcol, b);
@@ -435,7 +442,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         }
       }
     }
-  } else if (warp >= 12) {
+  } else if (warp >= 4 + 4 * NG) {
     // ------------------------------------------------ dQ drain (TMEM lane = query row)
     // dQ(t) -> swizzled smem staging (two 32-column chunks at a time) -> TMA bulk reduce-add
     // (fp32) into the circulating dQ; TMEM is released (dq_free) as soon as it has been read.
