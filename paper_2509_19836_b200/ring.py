@@ -24,7 +24,7 @@ hop is one NVLink traversal, so both are the same bandwidth class.
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import torch
 import torch.distributed as dist
@@ -47,6 +47,7 @@ def ring_schedule(topology: Topology, rank: int) -> list[int]:
 class RingStats:
     bytes_sent: int = 0
     launches: int = 0
+    kernel_events: list = field(default_factory=list)  # (start, end) CUDA events when recording
 
 
 class ProcessRing:
@@ -70,6 +71,25 @@ class ProcessRing:
         self.dmask = K.device_mask(mask, self.device)  # (host-side tests swap K for a CPU double)
         self.head_dim = head_dim
         self.stats = RingStats()
+        self.compute = True  # False: run only the exchanges (communication-alone timing)
+        self.record = False  # True: CUDA events around every kernel launch (compute-lane time)
+
+    def _launch(self, fn, *a, **kw):
+        if not self.compute:
+            return
+        if self.record:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn(*a, **kw)
+            e1.record()
+            self.stats.kernel_events.append((e0, e1))
+        else:
+            fn(*a, **kw)
+        self.stats.launches += 1
+
+    def kernel_seconds(self) -> float:
+        """Sum of recorded kernel durations (call after synchronizing)."""
+        return sum(a.elapsed_time(b) for a, b in self.stats.kernel_events) / 1e3
 
     # -------------------------------------------------------------- helpers
     def _peer(self, t: int) -> tuple[int, int]:
@@ -91,8 +111,22 @@ class ProcessRing:
         return 1.0 / math.sqrt(self.head_dim or d_pad)
 
     # -------------------------------------------------------------- forward
-    def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor | None = None, lse: torch.Tensor | None = None):
+    def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor | None = None,
+                lse: torch.Tensor | None = None, n_q: int | None = None):
+        """Ring forward.  ``n_q`` < n runs only the first n_q query rows (the rows a
+        sequence-selective checkpoint dropped, see ``recompute``); K/V still circulate whole."""
         n, hq, d = q.shape
+        if n_q is not None and n_q < n:
+            o_full = torch.zeros(n, hq, d, dtype=torch.float32, device=q.device) if o is None else o
+            lse_full = torch.full((hq, n), float("-inf"), device=q.device) if lse is None else lse
+            saved = self.compute
+            self.compute = saved and n_q > 0  # the exchanges are collective: always run them
+            try:
+                o_p, lse_p = self.forward(q[:n_q].contiguous(), k, v, o_full[:n_q], None)
+            finally:
+                self.compute = saved
+            lse_full[:, :n_q].copy_(lse_p)
+            return o_full, lse_full
         o = torch.zeros(n, hq, d, dtype=torch.float32, device=q.device) if o is None else o.zero_()
         lse = torch.full((hq, n), float("-inf"), device=q.device) if lse is None else lse.fill_(float("-inf"))
         bufs = [(k, v)] + [(torch.empty_like(k), torch.empty_like(v)) for _ in range(2)]
@@ -109,17 +143,26 @@ class ProcessRing:
                 nxt = bufs[1 + t % 2]
                 pending = self._exchange([k, v], list(nxt), dst, src)
             if self.counts[self.rank, j]:
-                K.attn_fwd_step(q, kv[0], kv[1], o, lse, self.layout, self.dmask, self.rank + 1, j + 1, self._scale(d))
-                self.stats.launches += 1
+                self._launch(K.attn_fwd_step, q, kv[0], kv[1], o, lse, self.layout, self.dmask, self.rank + 1, j + 1,
+                             self._scale(d), n_q=q.shape[0])
         return o, lse
+
+    def recompute(self, q, k, v, o, lse, policy) -> int:
+        """Sequence-selective checkpointing (checkpointing.py:141-157): recompute (O, lse) for this
+        rank's rows with global token id <= boundary -- a prefix of the shard -- with the ring
+        forward restricted to them.  Returns the number of recomputed rows."""
+        from .checkpointing import _prefix_rows
+
+        p = _prefix_rows(self.layout, policy.stored_from(self.layout.seq_len))[self.rank]
+        self.forward(q, k, v, o, lse, n_q=p)  # collective: every rank takes part, p may be 0
+        return p
 
     # -------------------------------------------------------------- backward
     def backward(self, q, k, v, do, o, lse, kind: str = BURST_BACKWARD, dq=None, dk=None, dv=None):
         """Gradients of sum(O * dO); ``kind`` picks the payload that circulates."""
         n, hq, d = q.shape
         delta = torch.empty_like(lse)
-        K.bwd_preprocess(do, o, delta)
-        self.stats.launches += 1
+        self._launch(K.bwd_preprocess, do, o, delta)
         dq = torch.zeros(q.shape, dtype=torch.float32, device=q.device) if dq is None else dq.zero_()
         dk = torch.zeros(k.shape, dtype=torch.float32, device=q.device) if dk is None else dk.zero_()
         dv = torch.zeros(v.shape, dtype=torch.float32, device=q.device) if dv is None else dv.zero_()
@@ -159,9 +202,8 @@ class ProcessRing:
                     grad_pending = None
                 acc.zero_()
             if self.counts[j, self.rank]:
-                K.attn_bwd_step(payload[0], k, v, payload[1], payload[2], payload[3], acc, dk, dv,
-                                self.layout, self.dmask, j + 1, self.rank + 1, self._scale(d))
-                self.stats.launches += 1
+                self._launch(K.attn_bwd_step, payload[0], k, v, payload[1], payload[2], payload[3], acc, dk, dv,
+                             self.layout, self.dmask, j + 1, self.rank + 1, self._scale(d))
             if t > 0:  # delayed gradient send: my partial for shard j goes to its owner j;
                 # I receive the partial for MY shard from the rank that computed it at step t
                 if grad_pending is not None:
@@ -206,9 +248,8 @@ class ProcessRing:
                 acc[0].zero_()
                 acc[1].zero_()
             if self.counts[self.rank, j]:
-                K.attn_bwd_step(q, kv[0], kv[1], do, lse, delta, dq, acc[0], acc[1],
-                                self.layout, self.dmask, self.rank + 1, j + 1, self._scale(d))
-                self.stats.launches += 1
+                self._launch(K.attn_bwd_step, q, kv[0], kv[1], do, lse, delta, dq, acc[0], acc[1],
+                             self.layout, self.dmask, self.rank + 1, j + 1, self._scale(d))
             if t > 0:
                 if grad_pending is not None:
                     for w in grad_pending[0]:

@@ -99,6 +99,17 @@ def _worker(rank, world, port, case, out_q):
         o, lse = ring.forward(q[rows].contiguous(), k[rows].contiguous(), v[rows].contiguous())
         dq, dk, dv = ring.backward(q[rows].contiguous(), k[rows].contiguous(), v[rows].contiguous(),
                                    do[rows].contiguous(), o, lse, kind=backward)
+        # sequence-selective checkpoint: drop (O, lse) of rows with id <= N/2, recompute them
+        from paper_2509_19836_b200.checkpointing import CheckpointPolicy
+
+        o2, lse2 = o.clone(), lse.clone()
+        o2.zero_()
+        lse2.fill_(float("nan"))
+        pol = CheckpointPolicy("sequence_selective", 0.5)
+        p_rows = ring.recompute(q[rows].contiguous(), k[rows].contiguous(), v[rows].contiguous(), o2, lse2, pol)
+        ids = device_token_ids(layout, rank + 1)
+        assert p_rows == int((ids <= n // 2).sum())
+        assert torch.allclose(o2[:p_rows], o[:p_rows]) and torch.allclose(lse2[:, :p_rows], lse[:, :p_rows])
         out_q.put((rank, rows.numpy(), o.numpy(), lse.numpy(), dq.numpy(), dk.numpy(), dv.numpy(), ring.stats.bytes_sent))
     finally:
         dist.destroy_process_group()
