@@ -247,7 +247,11 @@ def run_gpu(args) -> None:
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # High-priority NCCL streams: the attention kernels hold every SM (one 512-thread CTA per
+        # SM), so NCCL's P2P CTAs must win the next free SM or the ring exchange runs late.
+        opts = dist.ProcessGroupNCCL.Options()
+        opts.is_high_priority_stream = os.environ.get("BB_NCCL_HIGH_PRIORITY", "1") == "1"
+        dist.init_process_group("nccl", device_id=dev, pg_options=opts)
     from paper_2509_19836_b200 import _native
     from paper_2509_19836_b200 import kernels as K
     from paper_2509_19836_b200.fabric import Topology

@@ -24,7 +24,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    opts = dist.ProcessGroupNCCL.Options()
+    opts.is_high_priority_stream = True  # see bench.py: NCCL P2P CTAs must win free SMs
+    dist.init_process_group("nccl", device_id=dev, pg_options=opts)
     from oracle import burst_oracle as O
 
     failures = 0
