@@ -10,12 +10,13 @@
 // through a 3-slot TMA ring and are shared by both query tiles.
 //   warp 0      TMA producer (Q once, then K_j, V_j)
 //   warp 1      MMA issuer: S_k = Q_k K_j^T (SS, M=128,N=128) and
-//               O_k += P_k V_j (SS, M=128, N=D, V MN-major) into TMEM
+//               O_k += P_k V_j (TS: P read from TMEM, V MN-major from smem) into TMEM
 //   warp 2      TMEM allocator
 //   warps 4-7   softmax for query tile 0, warps 8-11 for query tile 1:
 //               one thread per row, online softmax in the log2 domain with a
-//               lazy (threshold 8) rescale of the TMEM O accumulator, P written
-//               to shared memory in the UMMA SWIZZLE_128B K-major layout.
+//               lazy (threshold 8) rescale of the TMEM O accumulator, P (bf16)
+//               written back over its own S columns in TMEM (tcgen05.st), where the
+//               P.V MMA reads it as the A operand -- no shared-memory round trip.
 // Tiles are classified from the closed-form id bounds (bb_mask.cuh): fully
 // masked tiles are never loaded or multiplied, fully visible tiles skip the
 // per-element predicate.
@@ -32,10 +33,19 @@ namespace {
 
 constexpr int FWD_THREADS = 384;
 constexpr int MAX_KT = 4096;  // key tiles per shard the class table holds (n_k <= 524288)
-constexpr int KV_SLOTS = 3;
+constexpr int KV_SLOTS = 5;
 constexpr float RESCALE_THRESHOLD = 8.0f;
 #ifndef BB_POLY_EVERY
 #define BB_POLY_EVERY 1000  // measured: any FMA-pipe share of exp2 was slower on B200
+#endif
+#ifndef BB_FWD_REGS
+#define BB_FWD_REGS 0  // setmaxnreg split measured: ptxas then spills far more (1.8 KB)
+#endif
+#ifndef BB_FWD_REGS_LO
+#define BB_FWD_REGS_LO 88
+#endif
+#ifndef BB_FWD_REGS_HI
+#define BB_FWD_REGS_HI 208
 #endif
 #ifndef BB_PACK_INT
 #define BB_PACK_INT 0
@@ -45,10 +55,8 @@ constexpr int POLY_EVERY = BB_POLY_EVERY;  // every POLY_EVERY-th P column uses 
 template <int D>
 struct FwdSmem {
   static constexpr uint32_t TILE = 128 * D * 2;  // one Q / K / V tile, D/64 panels of 16 KB
-  static constexpr uint32_t PTILE = 128 * 128 * 2;
   static constexpr uint32_t Q_OFF = 0;
-  static constexpr uint32_t P_OFF = Q_OFF + 2 * TILE;
-  static constexpr uint32_t KV_OFF = P_OFF + 2 * PTILE;
+  static constexpr uint32_t KV_OFF = Q_OFF + 2 * TILE;
   static constexpr uint32_t BAR_OFF = KV_OFF + KV_SLOTS * TILE;
   static constexpr uint32_t CLS_OFF = BAR_OFF + 256;  // per key tile: class(q tile 0) | class(q tile 1) << 2
   static constexpr uint32_t BYTES = CLS_OFF + MAX_KT / 2;  // 4 bits per key tile
@@ -91,12 +99,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;               // [3]
-  uint64_t* kv_empty = bars + 4;              // [3]
-  uint64_t* s_full = bars + 7;                // [2]
-  uint64_t* p_full = bars + 9;                // [2]
-  uint64_t* pv_done = bars + 11;              // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+  uint64_t* kv_full = bars + 1;                      // [KV_SLOTS]
+  uint64_t* kv_empty = bars + 1 + KV_SLOTS;          // [KV_SLOTS]
+  uint64_t* s_full = bars + 1 + 2 * KV_SLOTS;        // [2]
+  uint64_t* p_full = bars + 3 + 2 * KV_SLOTS;        // [2]
+  uint64_t* pv_done = bars + 5 + 2 * KV_SLOTS;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7 + 2 * KV_SLOTS);
 
   const int head = blockIdx.y;
   const int kv_head = head / (p.hq / p.hkv);
@@ -143,6 +151,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+#if BB_FWD_REGS
+  // producer / MMA warpgroup gives registers to the two softmax warpgroups (s[128] + P)
+  if (warp < 4)
+    setmaxnreg_dec<BB_FWD_REGS_LO>();
+  else
+    setmaxnreg_inc<BB_FWD_REGS_HI>();
+#endif
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
@@ -196,12 +211,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       mbar_wait(&p_full[q], issued[q] & 1);
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t p_base = smem_u32(smem + L::P_OFF + q * L::PTILE);
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-          const uint64_t ad = sw128_desc(p_base + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024);
+        for (int ks = 0; ks < 8; ++ks) {  // A = P: 16 keys (8 packed columns) per k-step
           const uint64_t bd = sw128_desc(v_base + ks * 2048, 16384, 1024);
-          umma_ss(tmem + (256u + q * D), ad, bd, idesc_o, (issued[q] | ks) != 0);
+          umma_ts(tmem + (256u + q * D), tmem + q * 128u + ks * 8u, bd, idesc_o, (issued[q] | ks) != 0);
         }
         umma_commit(&pv_done[q]);
       }
@@ -266,7 +279,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     const bool row_ok = qrow < p.n_q;
     const int64_t q_id = row_ok ? token_id(p.layout, p.q_device, qrow) : 0;
     const uint32_t t_lane = (quad * 32) << 16;
-    uint8_t* p_tile = smem + L::P_OFF + q * L::PTILE;
     const float sl2 = p.scale_log2;
 
     float m_run = -INFINITY, l_run = 0.f;
@@ -293,16 +305,17 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           if (!mask_bit(bits, c)) s[c] = -INFINITY;
       }
       if (row == 0) FWD_PROBE(t, 23 + 8 * q);
-      // Row max and row sum as 8-way trees (a 128-long dependent chain is ~512+ cycles).
+      // Row max as an 8-way tree of 3-input maxes (a 128-long dependent chain is ~512+ cycles).
       float mx8[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(s[i], s[i + 8]);
+      for (int i = 0; i < 8; ++i) mx8[i] = fmax3(s[i], s[i + 8], s[i + 16]);
 #pragma unroll
-      for (int c = 16; c < 128; c += 8)
+      for (int c = 24; c < 120; c += 16)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(mx8[i], s[c + i]);
-      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        for (int i = 0; i < 8; ++i) mx8[i] = fmax3(mx8[i], s[c + i], s[c + 8 + i]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(mx8[i], s[120 + i]);
+      const float mx = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
       const float m_tile = mx * sl2;
       const bool need = m_tile > m_run + RESCALE_THRESHOLD;
       float alpha = 1.f;
@@ -331,35 +344,34 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           tmem_st_wait();
         }
       }
-      // P = 2^(S*scale*log2e - m) on MUFU.  POLY_EVERY can move a share of the columns to a
-      // cubic on the FMA pipe (never for masked tiles, whose -inf scores need MUFU's exact 0);
-      // on B200 every share tried (1/8 .. 1/2) and integer bf16 packing measured slower, so
-      // the default keeps MUFU.EX2 + F2FP.
+      // P = 2^(S*scale*log2e - m), mostly on MUFU (16 lanes/clk/SM: 1024 clk per 128x128
+      // tile, the same as the tile's two MMAs).  POLY_EVERY moves a share of the columns to a
+      // cubic on the FMA pipe (never for masked tiles, whose -inf scores need MUFU's exact 0).
+      // P is packed to bf16x2 and stored over the S columns it came from, 32 keys at a time.
       float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       auto exp_pass = [&](auto masked_tag) {
         constexpr bool MASKED = decltype(masked_tag)::value;
 #pragma unroll
-        for (int c = 0; c < 128; c += 8) {
-          float e[8];
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t pk[16];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float x = fmaf(s[c + i], sl2, neg_m);
-            e[i] = (!MASKED && (i % POLY_EVERY) == POLY_EVERY - 1) ? ex2_poly(x) : ex2_approx(x);
-            acc8[i] += e[i];
-          }
-          uint4 pk;
+          for (int h = 0; h < 32; h += 8) {
+            float e[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float x = fmaf(s[c + h + i], sl2, neg_m);
+              e[i] = (!MASKED && (i % POLY_EVERY) == POLY_EVERY - 1) ? ex2_poly(x) : ex2_approx(x);
+              acc8[i] += e[i];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
 #if BB_PACK_INT
-          pk.x = pack_bf16_int(e[0], e[1]);
-          pk.y = pack_bf16_int(e[2], e[3]);
-          pk.z = pack_bf16_int(e[4], e[5]);
-          pk.w = pack_bf16_int(e[6], e[7]);
+              pk[h / 2 + i] = pack_bf16_int(e[2 * i], e[2 * i + 1]);
 #else
-          pk.x = pack_bf16(e[0], e[1]);
-          pk.y = pack_bf16(e[2], e[3]);
-          pk.z = pack_bf16(e[4], e[5]);
-          pk.w = pack_bf16(e[6], e[7]);
+              pk[h / 2 + i] = pack_bf16(e[2 * i], e[2 * i + 1]);
 #endif
-          *reinterpret_cast<uint4*>(p_tile + sw128_offset(row, c, 16384)) = pk;
+          }
+          tmem_st16(tmem + t_lane + q * 128u + c / 2, pk);
         }
       };
       if (cls == TILE_PARTIAL)
@@ -368,7 +380,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         exp_pass(std::false_type{});
       l_run += ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
       if (row == 0) FWD_PROBE(t, 20 + 8 * q);
-      fence_async_smem();
+      tmem_st_wait();
       if (row == 0) FWD_PROBE(t, 21 + 8 * q);
       tc_fence_before();
       mbar_arrive(&p_full[q]);

@@ -234,6 +234,23 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Per-warpgroup register rebalancing (all four warps of a warpgroup execute the same one).
+template <uint32_t kRegs>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+template <uint32_t kRegs>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+
+// Three-input max (FMNMX3, sm_100+): halves the instructions of a row-max tree.
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -257,7 +274,8 @@ __device__ __forceinline__ float ex2_poly(float x) {
 }
 
 // bf16x2 pack of two non-negative finite floats by integer rounding (half-up) on the ALU
-// pipe: 2 IADD + 1 PRMT instead of an F2FP on the 16-lane conversion pipe.
+// pipe: 2 IADD + 1 PRMT instead of one F2FP (tools/ubench_pipes.cu: F2FP runs at ~64
+// lanes/clk/SM and does not share MUFU's pipe, so this is kept only as an option).
 __device__ __forceinline__ uint32_t pack_bf16_int(float lo, float hi) {
   return __byte_perm(__float_as_uint(lo) + 0x8000u, __float_as_uint(hi) + 0x8000u, 0x7632);
 }
