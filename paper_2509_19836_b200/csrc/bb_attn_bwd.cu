@@ -26,6 +26,8 @@
 // TMEM: S^T / P^T [0,128), dP^T then dQ [128,256), dV [256,256+D), dK [256+D,256+2D).
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "bb_host.h"
 #include "bb_mask.cuh"
 #include "bb_ptx.cuh"
@@ -36,15 +38,13 @@ namespace {
 #ifndef BB_BWD_NG
 #define BB_BWD_NG 2
 #endif
-constexpr int NG = BB_BWD_NG;              // compute column groups (4 warps each)
+constexpr int NG = BB_BWD_NG;
+              // compute column groups (4 warps each)
 constexpr int CPG = 128 / NG;              // query columns per group
 constexpr int CH = CPG / 32;               // 32-column chunks per group
 constexpr int NCOMP = NG * 128;            // compute threads
 constexpr int BWD_THREADS = 128 + NCOMP + 128;  // control warps + compute + dQ drain
 constexpr int MAX_QT = 4096;  // query tiles per shard the class table holds (n_q <= 524288)
-#ifndef BB_DQ_RED
-#define BB_DQ_RED 0  // 1: dQ via red.global.add.v4.f32 from registers; 0: smem staging + TMA reduce-add
-#endif
 
 template <int D>
 struct BwdSmem {
@@ -110,7 +110,14 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint64_t* dq_full = bars + 11;
   uint64_t* dq_free = bars + 12;
   uint64_t* acc_full = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  // The dP^T / dQ columns are handed over in two 64-column halves: dQ half h (head dims
+  // [64h, 64h+64)) and dP^T half g (query columns of compute group g) share TMEM columns
+  // COL_DP + 64h, so dP_g(t+1) goes as soon as the drain has read dQ half g of tile t.
+  //   dp_full[g] = bars 9 / 14, dq_full[h] = bars 11 / 15, dq_free[h] = bars 12 / 16
+  uint64_t* dp_full2[2] = {bars + 9, bars + 14};
+  uint64_t* dq_full2[2] = {bars + 11, bars + 15};
+  uint64_t* dq_free2[2] = {bars + 12, bars + 16};
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
   float* vec_s = reinterpret_cast<float*>(smem + L::VEC_OFF);
 
   const int kv_head = blockIdx.y;
@@ -143,6 +150,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     mbar_init(s_full, 1);
     mbar_init(p_full, NCOMP);
     mbar_init(dp_full, 1);
+    mbar_init(dp_full2[1], 1);
+    mbar_init(dq_full2[1], 1);
+    mbar_init(dq_free2[1], 128);
     mbar_init(ds_full, NCOMP);
     mbar_init(dq_full, 1);
     mbar_init(dq_free, 128);
@@ -215,7 +225,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     // start P(t+1) while dK(t)/dQ(t) run and the drain warps empty dQ(t).
     constexpr uint32_t idesc_st = idesc_bf16(128, 128, false, false);  // S^T, dP^T
     constexpr uint32_t idesc_acc = idesc_bf16(128, D, false, true);    // dV (TS), dK: B MN-major
-    constexpr uint32_t idesc_dq = idesc_bf16(128, D, true, true);      // dQ: A = dS (MN), B = K (MN)
     const uint32_t k_base = smem_u32(smem + L::K_OFF), v_base = smem_u32(smem + L::V_OFF);
     const uint32_t do_base = smem_u32(smem + L::DO_OFF), ds_base = smem_u32(smem + L::DS_OFF);
     auto issue_s = [&](uint32_t qs) {
@@ -230,17 +239,21 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
       __syncwarp();
     };
-    auto issue_dp = [&]() {
+    constexpr uint32_t idesc_st64 = idesc_bf16(128, 64, false, false);  // dP^T half: 64 query columns
+    constexpr uint32_t idesc_dq64 = idesc_bf16(128, 64, true, true);    // dQ half: 64 head dims
+    auto issue_dp_half = [&](int g) {  // dP^T[:, 64g:64g+64] = V . dO[64g:64g+64]^T
       if (elect_one()) {
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
           const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
-          umma_ss(tmem + COL_DP, sw128_desc(v_base + off, 16, 1024), sw128_desc(do_base + off, 16, 1024), idesc_st, ks > 0);
+          umma_ss(tmem + COL_DP + 64 * g, sw128_desc(v_base + off, 16, 1024),
+                  sw128_desc(do_base + off + 8192 * g, 16, 1024), idesc_st64, ks > 0);
         }
-        umma_commit(dp_full);
+        umma_commit(dp_full2[g]);
       }
       __syncwarp();
     };
+
     mbar_wait(kv_full, 0);
     int64_t w = next_active(0);
     if (w < n_work) {
@@ -249,7 +262,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       issue_s(0);
       mbar_wait(do_full, 0);
       tc_fence_after();
-      issue_dp();
+      issue_dp_half(0);
+      issue_dp_half(1);
     }
     for (uint32_t it = 0; w < n_work; ++it) {
       const int64_t wn = next_active(w + 1);
@@ -265,7 +279,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           const uint32_t a_tmem = tmem + COL_S + (ks >> 1) * 32 + (ks & 1) * 8;  // P of q chunk c in its own S columns
           umma_ts(tmem + COL_DV, a_tmem, sw128_desc(do_base + ks * 2048, 16384, 1024), idesc_acc, (it | ks) != 0);
         }
-        umma_commit(do_empty);
+        umma_commit(do_empty);  // dP(t) and dV(t) have read dO(t)
       }
       __syncwarp();
       if (wn < n_work) {
@@ -285,20 +299,27 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         }
         umma_commit(&q_empty[qs]);
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {  // K = 128 keys
-          umma_ss(tmem + COL_DP, sw128_desc(ds_base + ks * 2048, 16384, 1024), sw128_desc(k_base + ks * 2048, 16384, 1024),
-                  idesc_dq, ks > 0);
+        for (int h = 0; h < D / 64; ++h) {
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)  // K = 128 keys; N = head dims [64h, 64h+64)
+            umma_ss(tmem + COL_DP + 64 * h, sw128_desc(ds_base + ks * 2048, 16384, 1024),
+                    sw128_desc(k_base + ks * 2048 + 16384 * h, 16384, 1024), idesc_dq64, ks > 0);
+          umma_commit(dq_full2[h]);
         }
-        umma_commit(dq_full);
       }
       __syncwarp();
       if (wn < n_work) {
         mbar_wait(do_full, (it + 1) & 1);
         if (lane == 0) BB_PROBE(6);
-        mbar_wait(dq_free, it & 1);  // dP^T columns held dQ(t)
-        if (lane == 0) BB_PROBE(7);
-        tc_fence_after();
-        issue_dp();
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          if (64 * g < D) {  // these dP^T columns held dQ half g of tile t
+            mbar_wait(dq_free2[g], it & 1);
+            tc_fence_after();
+          }
+          if (lane == 0 && g == 0) BB_PROBE(7);
+          issue_dp_half(g);
+        }
       }
       w = wn;
     }
@@ -313,6 +334,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     const uint32_t t_lane = (quad * 32) << 16;
     const int64_t krow = c0 + row;
     const bool key_ok = krow < p.n_k;
+    const bool ragged_k = c0 + 128 > p.n_k;  // CTA-uniform: the last key tile of a ragged shard
     const int64_t k_id = key_ok ? token_id(p.layout, p.k_device, krow) : 0;
     uint8_t* ds_tile = smem + L::DS_OFF;
 
@@ -349,54 +371,73 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       if (ct == 0) BB_PROBE(17);
       tc_fence_after();
 
-      // ---- P^T = exp2(S^T * scale*log2e - lse2[q]) -> TMEM (bf16 pairs, over S^T); kept packed
+      // ---- P^T = exp2(S^T * scale*log2e - lse2[q]) -> TMEM (bf16 pairs, over S^T); kept packed.
+      // lse2 of a 32-query chunk is read from smem before the TMEM load so the LDS latency
+      // hides under it (tcgen05.wait::ld is a compiler memory barrier).  Only partial tiles
+      // (and a ragged last key tile) pay for the per-element mask.
       uint32_t pk[CH][16];
+      auto p_pass = [&](auto masked_tag) {
+        constexpr bool MASKED = decltype(masked_tag)::value;
 #pragma unroll
-      for (int c2 = 0; c2 < CH; ++c2) {
-        const int c = g * CH + c2;
-        float s[32];
-        tmem_ld32(tmem + t_lane + COL_S + c * 32, s);
-        tmem_ld_wait();
+        for (int c2 = 0; c2 < CH; ++c2) {
+          const int c = g * CH + c2;
+          float l2[32];
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const int qc = c * 32 + i;
-          const float e0 = ex2_approx(fmaf(s[i], p.scale_log2, -lse2[qc]));
-          const float e1 = ex2_approx(fmaf(s[i + 1], p.scale_log2, -lse2[qc + 1]));
-          pk[c2][i / 2] = pack_bf16(mask_bit(bits, qc) ? e0 : 0.f, mask_bit(bits, qc + 1) ? e1 : 0.f);
+          for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(&l2[i]) = *reinterpret_cast<const float4*>(&lse2[c * 32 + i]);
+          float s[32];
+          tmem_ld32(tmem + t_lane + COL_S + c * 32, s);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const int qc = c * 32 + i;
+            float e0 = ex2_approx(fmaf(s[i], p.scale_log2, -l2[i]));
+            float e1 = ex2_approx(fmaf(s[i + 1], p.scale_log2, -l2[i + 1]));
+            if (MASKED) {
+              e0 = mask_bit(bits, qc) ? e0 : 0.f;
+              e1 = mask_bit(bits, qc + 1) ? e1 : 0.f;
+            }
+            pk[c2][i / 2] = pack_bf16(e0, e1);
+          }
+          tmem_st16(tmem + t_lane + COL_S + c * 32, pk[c2]);
         }
-        tmem_st16(tmem + t_lane + COL_S + c * 32, pk[c2]);
-      }
+      };
+      if (cls == TILE_PARTIAL || ragged_k)
+        p_pass(std::true_type{});
+      else
+        p_pass(std::false_type{});
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(p_full);
       if (ct == 0) BB_PROBE(18);
 
       // ---- dS^T = P^T o (dP^T - D[q]) -> smem (K-major rows = keys); the dK/dQ MMAs of the
-      // previous tile must have finished reading the buffer (dq_full(t-1)).
-      if (it > 0) mbar_wait(dq_full, (it - 1) & 1);
-      mbar_wait(dp_full, it & 1);
+      // previous tile must have finished reading the buffer: dP_g(t) is issued after dK(t-1)
+      // and dQ(t-1), so its commit covers them.
+      mbar_wait(dp_full2[NG == 2 ? g : 1], it & 1);
+      if (NG != 2) mbar_wait(dp_full2[0], it & 1);
       if (ct == 0) BB_PROBE(19);
       tc_fence_after();
 #pragma unroll
       for (int c2 = 0; c2 < CH; ++c2) {
         const int c = g * CH + c2;
+        float dl[32];
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(&dl[i]) = *reinterpret_cast<const float4*>(&dlt[c * 32 + i]);
         float dp[32];
         tmem_ld32(tmem + t_lane + COL_DP + c * 32, dp);
         tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          uint4 v;
-          uint32_t* vw = reinterpret_cast<uint32_t*>(&v);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int a = i + 2 * e;
-            const __nv_bfloat162 pb = *reinterpret_cast<const __nv_bfloat162*>(&pk[c2][a / 2]);
-            vw[e] = pack_bf16(__low2float(pb) * (dp[a] - dlt[c * 32 + a]),
-                              __high2float(pb) * (dp[a + 1] - dlt[c * 32 + a + 1]));
-          }
-          *reinterpret_cast<uint4*>(ds_tile + sw128_offset(row, c * 32 + i, 16384)) = v;
+        for (int a = 0; a < 32; a += 2) {  // dS^T packed in place of P^T
+          const __nv_bfloat162 pb = *reinterpret_cast<const __nv_bfloat162*>(&pk[c2][a / 2]);
+          pk[c2][a / 2] = pack_bf16(__low2float(pb) * (dp[a] - dl[a]), __high2float(pb) * (dp[a + 1] - dl[a + 1]));
         }
       }
+#pragma unroll
+      for (int c2 = 0; c2 < CH; ++c2)
+#pragma unroll
+        for (int i = 0; i < 32; i += 8)
+          *reinterpret_cast<uint4*>(ds_tile + sw128_offset(row, (g * CH + c2) * 32 + i, 16384)) =
+              make_uint4(pk[c2][i / 2], pk[c2][i / 2 + 1], pk[c2][i / 2 + 2], pk[c2][i / 2 + 3]);
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(ds_full);
@@ -445,7 +486,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   } else if (warp >= 4 + 4 * NG) {
     // ------------------------------------------------ dQ drain (TMEM lane = query row)
     // dQ(t) -> swizzled smem staging (two 32-column chunks at a time) -> TMA bulk reduce-add
-    // (fp32) into the circulating dQ; TMEM is released (dq_free) as soon as it has been read.
+    // (fp32) into the circulating dQ; each TMEM half is released (dq_free) as soon as it has
+    // been read.
     const uint32_t quad = warp & 3;
     const int row = quad * 32 + lane;
     const uint32_t t_lane = (quad * 32) << 16;
@@ -464,19 +506,17 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     for (int64_t w = next_active(0); w < n_work; w = next_active(w + 1), ++it) {
       const int32_t qrow0 = static_cast<int32_t>(item_qt(w) * 128);
       const int hcol = item_head(w) * D;
-      mbar_wait(dq_full, it & 1);
       if (row == 0) BB_PROBE(21);
-      tc_fence_after();
 #pragma unroll
       for (int half = 0; half < CHUNKS / 2; ++half) {
+        mbar_wait(dq_full2[half], it & 1);
+        tc_fence_after();
         float a[32], b[32];
         tmem_ld32(tmem + t_lane + COL_DP + half * 64, a);
         tmem_ld32(tmem + t_lane + COL_DP + half * 64 + 32, b);
         tmem_ld_wait();
-        if (half == CHUNKS / 2 - 1) {  // all of dQ(t) read: release its TMEM columns
-          tc_fence_before();
-          mbar_arrive(dq_free);
-        }
+        tc_fence_before();  // this half of dQ(t) is read: release its TMEM columns
+        mbar_arrive(dq_free2[half]);
         if (issuer) bulk_wait_read<0>();  // previous reduce finished reading the staging
         named_bar_sync(4, 128);
         stage(a, 0);

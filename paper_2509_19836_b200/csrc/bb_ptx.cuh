@@ -73,6 +73,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// Warm L2 with a 2-D tensor-map box (no smem destination, no completion tracking).
+__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
 // shared -> global element-wise fp32 add of a 2-D tensor-map box (bulk-group completion).
 __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src,
                                                   int32_t c0, int32_t c1) {
