@@ -265,3 +265,46 @@ def test_checkpoint_distributed_zigzag_front_blocks(cuda):
     bb.recompute_checkpointed(st, layout, bb.causal_mask())
     for s, o, l in zip(st, o_full, lse_full):
         assert torch.equal(s.o, o) and torch.equal(s.lse, l)  # same kernel, same rows: bitwise
+
+
+@pytest.mark.parametrize("g,kind,heads", [(1, "contiguous", (4, 4)), (4, "zigzag", (4, 4)), (4, "zigzag", (8, 2))])
+def test_error_within_2x_of_torch_bf16_sdpa(cuda, g, kind, heads):
+    """SURVEY §8(c) build tolerance: O error <= 2x the error of a bf16 library kernel (torch
+    SDPA, flash / cuDNN backend) against an fp64 reference on the same bf16 inputs; the same
+    bound is applied to dQ/dK/dV (relative Frobenius)."""
+    n, d = 2048, 128
+    hq, hkv = heads
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    q, k, v, do = ((torch.rand(n, h, d, device="cuda", generator=gen) * 2 - 1).to(torch.bfloat16) for h in (hq, hkv, hkv, hq))
+    # fp64 reference (autograd) on the bf16-quantised inputs, GQA by head repetition
+    rep = hq // hkv
+    q64, k64, v64 = (t.double().transpose(0, 1).requires_grad_() for t in (q, k, v))
+    s = (q64 @ k64.repeat_interleave(rep, 0).transpose(1, 2)) / math.sqrt(d)
+    s = s.masked_fill(torch.ones(n, n, dtype=torch.bool, device="cuda").triu(1), float("-inf"))
+    o64 = torch.softmax(s, -1) @ v64.repeat_interleave(rep, 0)
+    o64.backward(do.double().transpose(0, 1))
+    ref = {"o": o64.detach().transpose(0, 1), "dq": q64.grad.transpose(0, 1), "dk": k64.grad.transpose(0, 1), "dv": v64.grad.transpose(0, 1)}
+    # library bf16 kernel on the same inputs
+    qs, ks, vs = (t.transpose(0, 1).unsqueeze(0).detach().clone().requires_grad_() for t in (q, k, v))
+    os_ = torch.nn.functional.scaled_dot_product_attention(qs, ks, vs, is_causal=True, enable_gqa=rep > 1)
+    os_.backward(do.transpose(0, 1).unsqueeze(0))
+    lib = {"o": os_[0].detach().transpose(0, 1), "dq": qs.grad[0].transpose(0, 1), "dk": ks.grad[0].transpose(0, 1), "dv": vs.grad[0].transpose(0, 1)}
+    # this engine
+    layout = bb.ShardLayout(kind, n, g)
+    st = bb.make_device_states(layout, q, k, v)
+    bb.distributed_forward(st, layout, bb.causal_mask())
+    bb.burst_backward(st, bb.shard_rows(layout, do), layout, bb.causal_mask())
+    ours = {"o": bb.gather_rows(layout, [x.o for x in st])}
+    for name in ("dq", "dk", "dv"):
+        ours[name] = bb.gather_rows(layout, [getattr(x, name) for x in st])
+
+    def err(a, b, name):
+        a, b = a.double(), b.double()
+        if name == "o":
+            return float((a - b).abs().max())
+        return float(torch.linalg.norm(a - b) / torch.linalg.norm(b))
+
+    for name in ("o", "dq", "dk", "dv"):
+        e_ours, e_lib = err(ours[name], ref[name], name), err(lib[name], ref[name], name)
+        assert e_ours <= 2 * e_lib + 1e-6, (name, e_ours, e_lib)
+    assert err(ours["o"], ref["o"], "o") < TOL_O
