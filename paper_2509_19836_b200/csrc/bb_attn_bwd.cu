@@ -346,9 +346,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       const int64_t at = static_cast<int64_t>(item_head(w)) * p.n_q + r;
       return __ldg((ct < 128 ? p.lse : p.delta) + at);
     };
-    auto vec_val = [&](float raw) {  // lse -> lse*log2e (-inf row -> +inf so P = 0); delta as is
-      if (ct >= 128) return raw;
-      return raw == -INFINITY ? INFINITY : raw * 1.4426950408889634f;
+    auto vec_val = [&](float raw) {  // stored negated for the packed FFMA2 / FADD2 forms:
+      if (ct >= 128) return -raw;       //   -D,  and -lse*log2e (-inf row -> -inf, so P = 0)
+      return raw == -INFINITY ? -INFINITY : -raw * 1.4426950408889634f;
     };
 
     int64_t w = next_active(0);
@@ -390,8 +390,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
             const int qc = c * 32 + i;
-            float e0 = ex2_approx(fmaf(s[i], p.scale_log2, -l2[i]));
-            float e1 = ex2_approx(fmaf(s[i + 1], p.scale_log2, -l2[i + 1]));
+            const float2 x = __ffma2_rn(make_float2(s[i], s[i + 1]), make_float2(p.scale_log2, p.scale_log2),
+                                        make_float2(l2[i], l2[i + 1]));  // l2 = -lse*log2e
+            float e0 = ex2_approx(x.x);
+            float e1 = ex2_approx(x.y);
             if (MASKED) {
               e0 = mask_bit(bits, qc) ? e0 : 0.f;
               e1 = mask_bit(bits, qc + 1) ? e1 : 0.f;
@@ -429,7 +431,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 #pragma unroll
         for (int a = 0; a < 32; a += 2) {  // dS^T packed in place of P^T
           const __nv_bfloat162 pb = *reinterpret_cast<const __nv_bfloat162*>(&pk[c2][a / 2]);
-          pk[c2][a / 2] = pack_bf16(__low2float(pb) * (dp[a] - dl[a]), __high2float(pb) * (dp[a + 1] - dl[a + 1]));
+          const float2 ds = __fmul2_rn(__fadd2_rn(make_float2(dp[a], dp[a + 1]), make_float2(dl[a], dl[a + 1])),
+                                       make_float2(__low2float(pb), __high2float(pb)));  // dl = -D
+          pk[c2][a / 2] = pack_bf16(ds.x, ds.y);
         }
       }
 #pragma unroll

@@ -47,6 +47,9 @@ constexpr float RESCALE_THRESHOLD = 8.0f;
 #ifndef BB_FWD_REGS_HI
 #define BB_FWD_REGS_HI 208
 #endif
+#ifndef BB_FWD_X2
+#define BB_FWD_X2 1
+#endif
 #ifndef BB_PACK_INT
 #define BB_PACK_INT 0
 #endif
@@ -349,6 +352,32 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       // cubic on the FMA pipe (never for masked tiles, whose -inf scores need MUFU's exact 0).
       // P is packed to bf16x2 and stored over the S columns it came from, 32 keys at a time.
       float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#if BB_FWD_X2
+      // packed fp32x2 arithmetic (FFMA2 for the scale, FADD2 for the row sums): half the FP32
+      // issue slots of the scalar form; POLY_EVERY (in pairs) moves a share to ex2_poly2.
+      float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      const float2 sl2x2 = make_float2(sl2, sl2), negm2 = make_float2(neg_m, neg_m);
+      auto exp_pass = [&](auto masked_tag) {
+        constexpr bool MASKED = decltype(masked_tag)::value;
+#pragma unroll
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int h = 0; h < 32; h += 8) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 x = __ffma2_rn(make_float2(s[c + h + 2 * i], s[c + h + 2 * i + 1]), sl2x2, negm2);
+              const float2 e = (!MASKED && (i % POLY_EVERY) == POLY_EVERY - 1)
+                                   ? ex2_poly2(x)
+                                   : make_float2(ex2_approx(x.x), ex2_approx(x.y));
+              acc4[i] = __fadd2_rn(acc4[i], e);
+              pk[h / 2 + i] = pack_bf16(e.x, e.y);
+            }
+          }
+          tmem_st16(tmem + t_lane + q * 128u + c / 2, pk);
+        }
+      };
+#else
       auto exp_pass = [&](auto masked_tag) {
         constexpr bool MASKED = decltype(masked_tag)::value;
 #pragma unroll
@@ -374,10 +403,21 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           tmem_st16(tmem + t_lane + q * 128u + c / 2, pk);
         }
       };
+#endif
       if (cls == TILE_PARTIAL)
         exp_pass(std::true_type{});
       else
         exp_pass(std::false_type{});
+#if BB_FWD_X2
+      acc8[0] = acc4[0].x;
+      acc8[1] = acc4[0].y;
+      acc8[2] = acc4[1].x;
+      acc8[3] = acc4[1].y;
+      acc8[4] = acc4[2].x;
+      acc8[5] = acc4[2].y;
+      acc8[6] = acc4[3].x;
+      acc8[7] = acc4[3].y;
+#endif
       l_run += ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
       if (row == 0) FWD_PROBE(t, 20 + 8 * q);
       tmem_st_wait();

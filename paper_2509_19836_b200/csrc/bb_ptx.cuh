@@ -280,6 +280,23 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// 2^x for a pair on the packed fp32x2 FMA pipe (FADD2 / FFMA2, sm_100): j = floor(x) by a
+// round-down add of 1.5*2^23, a cubic in the fraction, 2^j added into the exponent field.
+// Inputs are clamped to >= -126 (masked -inf scores must go through MUFU instead).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 j = __fadd2_rd(x, magic);
+  const float2 f = __fadd2_rn(x, __fadd2_rn(magic, make_float2(-j.x, -j.y)));
+  float2 p = __ffma2_rn(make_float2(0.0555041086648216f, 0.0555041086648216f), f,
+                        make_float2(0.2402264923172231f, 0.2402264923172231f));
+  p = __ffma2_rn(p, f, make_float2(0.6931471805599453f, 0.6931471805599453f));
+  p = __ffma2_rn(p, f, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
+}
+
 // bf16x2 pack of two non-negative finite floats by integer rounding (half-up) on the ALU
 // pipe: 2 IADD + 1 PRMT instead of one F2FP (tools/ubench_pipes.cu: F2FP runs at ~64
 // lanes/clk/SM and does not share MUFU's pipe, so this is kept only as an option).

@@ -9,6 +9,22 @@
 
 using namespace bb;
 
+// 2^x for a pair on the packed FMA pipe: x = j + f, j = floor(x) via a round-down add of
+// 1.5*2^23, cubic in f, 2^j inserted into the exponent field with an integer add.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 j = __fadd2_rd(x, magic);
+  const float2 f = __fadd2_rn(x, __fadd2_rn(magic, make_float2(-j.x, -j.y)));
+  float2 p = __ffma2_rn(make_float2(0.0555041086648216f, 0.0555041086648216f), f,
+                        make_float2(0.2402264923172231f, 0.2402264923172231f));
+  p = __ffma2_rn(p, f, make_float2(0.6931471805599453f, 0.6931471805599453f));
+  p = __ffma2_rn(p, f, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
+}
+
 template <int COLS, int MODE>
 __global__ void __launch_bounds__(COLS == 128 ? 256 : 512, 1) sm_bench(float* out, long long* cyc, int iters, float sl2) {
   float s[COLS];
@@ -21,6 +37,29 @@ __global__ void __launch_bounds__(COLS == 128 ? 256 : 512, 1) sm_bench(float* ou
     const float neg_m = -0.5f - 1e-7f * it;
     float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     uint32_t pk[COLS / 2];
+    if (MODE >= 2) {  // packed fp32x2: FFMA2 for the scale, FADD2 for the row sums
+      float2 a4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      const float2 c2 = make_float2(sl2, sl2), m2 = make_float2(neg_m, neg_m);
+#pragma unroll
+      for (int c = 0; c < COLS; c += 8) {
+        float2 e[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 x = __ffma2_rn(make_float2(s[c + 2 * i], s[c + 2 * i + 1]), c2, m2);
+          if (MODE == 3 && i == 3) {
+            e[i] = ex2_poly2(x);
+          } else {
+            e[i] = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+          }
+          a4[i] = __fadd2_rn(a4[i], e[i]);
+          pk[c / 2 + i] = pack_bf16(e[i].x, e[i].y);
+        }
+      }
+      acc8[0] = a4[0].x + a4[0].y;
+      acc8[1] = a4[1].x + a4[1].y;
+      acc8[2] = a4[2].x + a4[2].y;
+      acc8[3] = a4[3].x + a4[3].y;
+    } else
 #pragma unroll
     for (int c = 0; c < COLS; c += 8) {
       float e[8];
@@ -52,7 +91,8 @@ void run(int warps, float* out, long long* cyc) {
     cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
   }
   const double elems = double(iters) * COLS * warps * 32;
-  printf("COLS %3d  warps/SM %2d  %-10s %6.0f clk per 16384 elements\n", COLS, warps, MODE ? "3:1 poly" : "MUFU",
+  const char* names[] = {"MUFU", "3:1 poly", "x2 MUFU", "x2 3:1 poly"};
+  printf("COLS %3d  warps/SM %2d  %-12s %6.0f clk per 16384 elements\n", COLS, warps, names[MODE],
          16384.0 * double(h) / elems);
 }
 
@@ -66,6 +106,10 @@ int main() {
     run<64, 0>(w, out, cyc);
     if (w <= 8) run<128, 1>(w, out, cyc);
     run<64, 1>(w, out, cyc);
+    if (w <= 8) run<128, 2>(w, out, cyc);
+    run<64, 2>(w, out, cyc);
+    if (w <= 8) run<128, 3>(w, out, cyc);
+    run<64, 3>(w, out, cyc);
   }
   return 0;
 }
