@@ -39,6 +39,9 @@ namespace {
 #define BB_BWD_NG 2
 #endif
 constexpr int NG = BB_BWD_NG;
+#ifndef BB_BWD_DQ128
+#define BB_BWD_DQ128 1
+#endif
               // compute column groups (4 warps each)
 constexpr int CPG = 128 / NG;              // query columns per group
 constexpr int CH = CPG / 32;               // 32-column chunks per group
@@ -241,6 +244,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     };
     constexpr uint32_t idesc_st64 = idesc_bf16(128, 64, false, false);  // dP^T half: 64 query columns
     constexpr uint32_t idesc_dq64 = idesc_bf16(128, 64, true, true);    // dQ half: 64 head dims
+    constexpr uint32_t idesc_dq = idesc_bf16(128, D, true, true);       // dQ: A = dS (MN), B = K (MN)
     auto issue_dp_half = [&](int g) {  // dP^T[:, 64g:64g+64] = V . dO[64g:64g+64]^T
       if (elect_one()) {
 #pragma unroll
@@ -298,6 +302,16 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           umma_ss(tmem + COL_DK, ad, sw128_desc(q_base + ks * 2048, 16384, 1024), idesc_acc, (it | ks) != 0);
         }
         umma_commit(&q_empty[qs]);
+#if BB_BWD_DQ128
+        // one N=D MMA group (N=64 instructions are issue-bound at ~48 clk vs 32 nominal,
+        // tools/ubench_mma_rate.cu); both halves become ready together
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)  // K = 128 keys
+          umma_ss(tmem + COL_DP, sw128_desc(ds_base + ks * 2048, 16384, 1024),
+                  sw128_desc(k_base + ks * 2048, 16384, 1024), idesc_dq, ks > 0);
+#pragma unroll
+        for (int h = 0; h < D / 64; ++h) umma_commit(dq_full2[h]);
+#else
 #pragma unroll
         for (int h = 0; h < D / 64; ++h) {
 #pragma unroll
@@ -306,6 +320,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                     sw128_desc(k_base + ks * 2048 + 16384 * h, 16384, 1024), idesc_dq64, ks > 0);
           umma_commit(dq_full2[h]);
         }
+#endif
       }
       __syncwarp();
       if (wn < n_work) {
