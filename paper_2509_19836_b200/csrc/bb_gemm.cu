@@ -4,7 +4,8 @@
 //
 // Tile 128 x 256 x 64, 4-stage TMA -> smem ring, one elected thread issues
 // tcgen05.mma (M=128, N=256, K=16 per instruction), four epilogue warps drain
-// TMEM with tcgen05.ld.  Operands may be K-major or MN-major (SWIZZLE_128B
+// TMEM with tcgen05.ld.  Persistent (one CTA per SM) with the accumulator
+// double-buffered in TMEM, so each tile's epilogue overlaps the next main loop.  Operands may be K-major or MN-major (SWIZZLE_128B
 // either way), which lets the three LM-head contractions run without any
 // transposed copies:
 //   logits = H  . W^T   (A=H  K-major,  B=W K-major)   lmhead.py:78
@@ -34,6 +35,9 @@ struct GemmArgs {
   bool raster_m_fast;
 };
 
+// Persistent: one CTA per SM walks tiles blockIdx.x, +gridDim.x, ...; the accumulator is
+// double-buffered in TMEM (2 x 256 columns) so tile i+1's main loop runs while the epilogue
+// warps drain tile i.
 template <bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
@@ -45,15 +49,19 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* sB = smem + STAGES * A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* done = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* acc_full = empty + STAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
-  const int tile = blockIdx.x;
-  const int tm = p.raster_m_fast ? tile % p.tiles_m : tile / p.tiles_n;
-  const int tn = p.raster_m_fast ? tile / p.tiles_m : tile % p.tiles_n;
-  const int m0 = tm * BM, n0 = tn * BN;
+  const int n_tiles = p.tiles_m * p.tiles_n;
   const int num_k = static_cast<int>((p.k + BK - 1) / BK);
   const uint32_t warp = warp_id(), lane = lane_id();
+  auto tile_mn = [&](int tile, int& m0, int& n0, int& tn) {
+    const int tm = p.raster_m_fast ? tile % p.tiles_m : tile / p.tiles_n;
+    tn = p.raster_m_fast ? tile / p.tiles_m : tile % p.tiles_n;
+    m0 = tm * BM;
+    n0 = tn * BN;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tma_a);
@@ -62,10 +70,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 128);
+    }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<256>(tmem_slot);
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -74,126 +85,149 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (elect_one()) {
-      for (int kb = 0; kb < num_k; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-        const int k0 = kb * BK;
-        uint8_t* a_dst = sA + s * A_BYTES;
-        uint8_t* b_dst = sB + s * B_BYTES;
-        if (!A_MN) {
-          tma_load_2d(a_dst, &tma_a, &full[s], k0, m0);
-        } else {
-          tma_load_2d(a_dst, &tma_a, &full[s], m0, k0);
-          tma_load_2d(a_dst + 8192, &tma_a, &full[s], m0 + 64, k0);
-        }
-        if (!B_MN) {
-          tma_load_2d(b_dst, &tma_b, &full[s], k0, n0);
-        } else {
+      uint32_t kc = 0;  // k-blocks issued so far (ring position)
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        int m0, n0, tn;
+        tile_mn(tile, m0, n0, tn);
+        for (int kb = 0; kb < num_k; ++kb, ++kc) {
+          const int s = kc % STAGES;
+          const uint32_t ph = (kc / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+          const int k0 = kb * BK;
+          uint8_t* a_dst = sA + s * A_BYTES;
+          uint8_t* b_dst = sB + s * B_BYTES;
+          if (!A_MN) {
+            tma_load_2d(a_dst, &tma_a, &full[s], k0, m0);
+          } else {
+            tma_load_2d(a_dst, &tma_a, &full[s], m0, k0);
+            tma_load_2d(a_dst + 8192, &tma_a, &full[s], m0 + 64, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d(b_dst, &tma_b, &full[s], k0, n0);
+          } else {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) tma_load_2d(b_dst + i * 8192, &tma_b, &full[s], n0 + 64 * i, k0);
+            for (int i = 0; i < 4; ++i) tma_load_2d(b_dst + i * 8192, &tma_b, &full[s], n0 + 64 * i, k0);
+          }
         }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
-    for (int kb = 0; kb < num_k; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      mbar_wait(&full[s], ph);
+    uint32_t kc = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+      const int buf = it & 1;
+      mbar_wait(&acc_empty[buf], ((it >> 1) & 1) ^ 1);  // epilogue has drained this buffer
       tc_fence_after();
-      if (elect_one()) {
-        const uint32_t a_base = smem_u32(sA + s * A_BYTES);
-        const uint32_t b_base = smem_u32(sB + s * B_BYTES);
+      const uint32_t acc = tmem + buf * BN;
+      for (int kb = 0; kb < num_k; ++kb, ++kc) {
+        const int s = kc % STAGES;
+        const uint32_t ph = (kc / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a_base = smem_u32(sA + s * A_BYTES);
+          const uint32_t b_base = smem_u32(sB + s * B_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {
-          const uint64_t ad = A_MN ? sw128_desc(a_base + kk * 2048, 8192, 1024)
-                                   : sw128_desc(a_base + kk * 32, 16, 1024);
-          const uint64_t bd = B_MN ? sw128_desc(b_base + kk * 2048, 8192, 1024)
-                                   : sw128_desc(b_base + kk * 32, 16, 1024);
-          umma_ss(tmem, ad, bd, idesc, (kb | kk) != 0);
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = A_MN ? sw128_desc(a_base + kk * 2048, 8192, 1024)
+                                     : sw128_desc(a_base + kk * 32, 16, 1024);
+            const uint64_t bd = B_MN ? sw128_desc(b_base + kk * 2048, 8192, 1024)
+                                     : sw128_desc(b_base + kk * 32, 16, 1024);
+            umma_ss(acc, ad, bd, idesc, (kb | kk) != 0);
+          }
+          umma_commit(&empty[s]);
+          if (kb == num_k - 1) umma_commit(&acc_full[buf]);
         }
-        umma_commit(&empty[s]);
-        if (kb == num_k - 1) umma_commit(done);
+        __syncwarp();
       }
-      __syncwarp();
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> registers -> global ----------------
     const uint32_t quad = warp & 3;
     const int row = quad * 32 + lane;
-    const int64_t grow = m0 + row;
-    mbar_wait(done, 0);
-    tc_fence_after();
-    const bool row_ok = grow < p.m;
-    float run_max = -INFINITY, run_sum = 0.f;
-    int64_t tgt = -1;
-    if (EPI == GEMM_LOGITS && row_ok) tgt = p.le.targets[grow] - n0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+      int m0, n0, tn;
+      tile_mn(tile, m0, n0, tn);
+      const int buf = it & 1;
+      const int64_t grow = m0 + row;
+      mbar_wait(&acc_full[buf], (it >> 1) & 1);
+      tc_fence_after();
+      const bool row_ok = grow < p.m;
+      float run_max = -INFINITY, run_sum = 0.f;
+      int64_t tgt = -1;
+      if (EPI == GEMM_LOGITS && row_ok) tgt = p.le.targets[grow] - n0;
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
-      float v[32];
-      tmem_ld32(tmem + ((quad * 32) << 16) + c * 32, v);
-      tmem_ld_wait();
-      const int64_t col0 = n0 + c * 32;
-      if (!row_ok || col0 >= p.n) continue;
-      float* dst = p.c ? p.c + grow * p.ldc + col0 : nullptr;
-      const bool full_chunk = col0 + 32 <= p.n;
-      if (EPI == GEMM_LOGITS) {
-        float cmax = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (full_chunk || col0 + i < p.n) cmax = fmaxf(cmax, v[i]);
-        const float nmax = fmaxf(run_max, cmax);
-        float s = 0.f;
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (full_chunk || col0 + i < p.n) s += __expf(v[i] - nmax);
-        run_sum = run_sum * __expf(run_max - nmax) + s;
-        run_max = nmax;
-        const int64_t t = tgt - c * 32;
-        if (t >= 0 && t < 32) {
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        tmem_ld32(tmem + ((quad * 32) << 16) + buf * BN + c * 32, v);
+        tmem_ld_wait();
+        if (c == BN / 32 - 1) {  // the whole accumulator is in registers: hand the buffer back
+          tc_fence_before();
+          mbar_arrive(&acc_empty[buf]);
+        }
+        const int64_t col0 = n0 + c * 32;
+        if (!row_ok || col0 >= p.n) continue;
+        float* dst = p.c ? p.c + grow * p.ldc + col0 : nullptr;
+        const bool full_chunk = col0 + 32 <= p.n;
+        if (EPI == GEMM_LOGITS) {
+          float cmax = -INFINITY;
 #pragma unroll
           for (int i = 0; i < 32; ++i)
-            if (i == t) p.le.tgt_logit[grow] = v[i];
-        }
-      }
-      if (dst) {
-        if (full_chunk && (p.ldc % 4) == 0) {
+            if (full_chunk || col0 + i < p.n) cmax = fmaxf(cmax, v[i]);
+          const float nmax = fmaxf(run_max, cmax);
+          float s = 0.f;
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            float4* d4 = reinterpret_cast<float4*>(dst + i);
-            if (EPI == GEMM_ACCUM) {
-              float4 o = *d4;
-              o.x += v[i];
-              o.y += v[i + 1];
-              o.z += v[i + 2];
-              o.w += v[i + 3];
-              *d4 = o;
-            } else {
-              *d4 = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          for (int i = 0; i < 32; ++i)
+            if (full_chunk || col0 + i < p.n) s += __expf(v[i] - nmax);
+          run_sum = run_sum * __expf(run_max - nmax) + s;
+          run_max = nmax;
+          const int64_t t = tgt - c * 32;
+          if (t >= 0 && t < 32) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i == t) p.le.tgt_logit[grow] = v[i];
+          }
+        }
+        if (dst) {
+          if (full_chunk && (p.ldc % 4) == 0) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              float4* d4 = reinterpret_cast<float4*>(dst + i);
+              if (EPI == GEMM_ACCUM) {
+                float4 o = *d4;
+                o.x += v[i];
+                o.y += v[i + 1];
+                o.z += v[i + 2];
+                o.w += v[i + 3];
+                *d4 = o;
+              } else {
+                *d4 = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+              }
+            }
+          } else {
+            for (int i = 0; i < 32 && col0 + i < p.n; ++i) {
+              if (EPI == GEMM_ACCUM)
+                dst[i] += v[i];
+              else
+                dst[i] = v[i];
             }
           }
-        } else {
-          for (int i = 0; i < 32 && col0 + i < p.n; ++i) {
-            if (EPI == GEMM_ACCUM)
-              dst[i] += v[i];
-            else
-              dst[i] = v[i];
-          }
         }
       }
-    }
-    if (EPI == GEMM_LOGITS && row_ok) {
-      p.le.part_max[grow * p.tiles_n + tn] = run_max;
-      p.le.part_sum[grow * p.tiles_n + tn] = run_sum;
+      if (EPI == GEMM_LOGITS && row_ok) {
+        p.le.part_max[grow * p.tiles_n + tn] = run_max;
+        p.le.part_sum[grow * p.tiles_n + tn] = run_sum;
+      }
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_dealloc<256>(tmem);
+  if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
 template <bool A_MN, bool B_MN, int EPI>
@@ -208,7 +242,10 @@ int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& ar
       return BB_ERR_CUDA;
     attr_done |= uint64_t(1) << dev;
   }
-  const int grid = args.tiles_m * args.tiles_n;
+  static int sms[64] = {0};
+  if (!sms[dev & 63]) cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+  const int tiles = args.tiles_m * args.tiles_n;
+  const int grid = tiles < sms[dev & 63] ? tiles : sms[dev & 63];
   kern<<<grid, THREADS, SMEM_BYTES, st>>>(ta, tb, args);
   return check_launch("gemm_kernel");
 }
