@@ -29,7 +29,7 @@ def _ref_attention(q, k, v, allowed, scale):
 
 
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
-@pytest.mark.parametrize("m,n,k", [(128, 256, 64), (304, 520, 200), (1024, 768, 4096)])
+@pytest.mark.parametrize("m,n,k", [(128, 256, 64), (304, 520, 200), (640, 1000, 320), (1024, 768, 4096)])
 def test_gemm_matches_torch(cuda, a_mn, b_mn, m, n, k):
     g = torch.Generator(device=cuda).manual_seed(m + n + k)
     a = torch.randn(m, k, device=cuda, generator=g).to(torch.bfloat16)
