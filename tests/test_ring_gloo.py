@@ -1,4 +1,4 @@
-"""Multi-process ring host logic on CPU (gloo, world sizes 2 and 4).
+"""Multi-process ring host logic on CPU (gloo, world sizes 2, 4 and 8).
 
 ProcessRing's schedule -- which shard each rank computes at each step, who sends
 it, and where every gradient partial goes -- is exercised for real over
@@ -121,6 +121,9 @@ CASES = [
     ("zigzag", 64, (1, 4), "causal", 2, 2, 8, "burst_backward"),
     ("striped", 64, (2, 2), "window", 4, 2, 8, "burst_backward"),
     ("contiguous", 64, (2, 2), "full", 2, 2, 4, "ring_backward"),
+    # the driver's 8-GPU scaling run: flat 1x8 and two-level 2x4 plans
+    ("zigzag", 128, (1, 8), "causal", 2, 2, 8, "burst_backward"),
+    ("striped", 128, (2, 4), "window", 2, 1, 8, "ring_backward"),
 ]
 
 
