@@ -39,6 +39,10 @@ namespace {
 #define BB_BWD_NG 2
 #endif
 constexpr int NG = BB_BWD_NG;
+#ifndef BB_BWD_MC
+#define BB_BWD_MC 1
+#endif
+constexpr bool MC = BB_BWD_MC;
 #ifndef BB_BWD_DQ128
 #define BB_BWD_DQ128 1
 #endif
@@ -126,11 +130,34 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   const int kv_head = blockIdx.y;
   const int group = p.hq / p.hkv;
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 128;  // low key tiles carry the most work
+  // MC: clusters of two adjacent key tiles share every Q / dO tile through a TMA multicast
+  // (half the L2 reads); both CTAs walk the union of their query ranges, and a query tile
+  // only one of them can see is computed by the other fully masked (P = 0).
+  const uint32_t crank = MC ? cluster_ctarank() : 0;
+  const int64_t c0p = c0 + (crank ? -128 : 128);  // the partner's key tile (MC)
+  auto q_range = [&](int64_t kc, int64_t& lo, int64_t& hi) {
+    lo = hi = 0;
+    if (kc < 0 || kc >= p.n_k) return;
+    active_runs(p.layout, p.mask, token_id(p.layout, p.k_device, kc),
+                token_id(p.layout, p.k_device, min(kc + 128, p.n_k) - 1), p.q_device, p.n_q, false, lo, hi);
+  };
   // Query tiles that can touch this key tile (two binary searches, every thread), then the
   // work items (query head of the GQA group, query tile in [q_lo, q_hi)).
   int64_t q_lo, q_hi;
-  active_runs(p.layout, p.mask, token_id(p.layout, p.k_device, c0),
-              token_id(p.layout, p.k_device, min(c0 + 128, p.n_k) - 1), p.q_device, p.n_q, false, q_lo, q_hi);
+  q_range(c0, q_lo, q_hi);
+  if (MC) {
+    int64_t p_lo, p_hi;
+    q_range(c0p, p_lo, p_hi);
+    if (p_hi > p_lo) {
+      if (q_hi > q_lo) {
+        q_lo = min(q_lo, p_lo);
+        q_hi = max(q_hi, p_hi);
+      } else {
+        q_lo = p_lo;
+        q_hi = p_hi;
+      }
+    }
+  }
   const uint32_t nr = static_cast<uint32_t>(q_hi - q_lo);
   // Work item w packs (head-in-group << 16 | query-tile index): no divisions on the roles'
   // per-tile path (a u32 div/mod is a ~100-cycle dependent chain).  n_work = end sentinel.
@@ -146,10 +173,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     mbar_init(kv_full, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&q_full[s], 1);
-      mbar_init(&q_empty[s], 1);
+      mbar_init(&q_empty[s], MC ? 2 : 1);  // MC: both CTAs' MMAs must have read the slot
     }
     mbar_init(do_full, 1);
-    mbar_init(do_empty, 1);
+    mbar_init(do_empty, MC ? 2 : 1);
     mbar_init(s_full, 1);
     mbar_init(p_full, NCOMP);
     mbar_init(dp_full, 1);
@@ -170,7 +197,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   for (uint32_t b = threadIdx.x; b < (nr + 3) / 4; b += BWD_THREADS) {
     uint32_t byte = 0;
     for (uint32_t k = 0; k < 4; ++k)
-      if (4 * b + k < nr) byte |= static_cast<uint32_t>(bwd_class(p, q_lo + 4 * b + k, c0)) << (2 * k);
+      if (4 * b + k < nr) {
+        const int64_t qt = q_lo + 4 * b + k;
+        int32_t cls = c0 < p.n_k ? bwd_class(p, qt, c0) : TILE_SKIP;
+        if (MC && cls == TILE_SKIP && c0p >= 0 && c0p < p.n_k && bwd_class(p, qt, c0p) != TILE_SKIP)
+          cls = TILE_PARTIAL;  // the partner needs this tile: compute it fully masked
+        byte |= static_cast<uint32_t>(cls) << (2 * k);
+      }
     cls_tab[b] = static_cast<uint8_t>(byte);
   }
   auto tile_cls = [&](uint32_t qt) {
@@ -178,7 +211,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     return static_cast<int32_t>((cls_tab[x >> 2] >> ((x & 3) * 2)) & 3);
   };
   tc_fence_before();
-  __syncthreads();
+  if (MC)
+    cluster_sync();  // the partner's multicasts may target this CTA's barriers from here on
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -211,13 +247,20 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         mbar_wait(&q_empty[qs], ((it >> 1) & 1) ^ 1);
         BB_PROBE(1);
         mbar_expect_tx(&q_full[qs], L::TILE);
-        for (int pn = 0; pn < PANELS; ++pn)
-          tma_load_2d(smem + L::Q_OFF + qs * L::TILE + pn * 16384, &tq, &q_full[qs], h * D + pn * 64, qrow0);
+        for (int pn = 0; pn < PANELS; ++pn) {
+          if (!MC)
+            tma_load_2d(smem + L::Q_OFF + qs * L::TILE + pn * 16384, &tq, &q_full[qs], h * D + pn * 64, qrow0);
+          else if (crank == 0)
+            tma_load_2d_mc(smem + L::Q_OFF + qs * L::TILE + pn * 16384, &tq, &q_full[qs], h * D + pn * 64, qrow0, 3);
+        }
         mbar_wait(do_empty, (it & 1) ^ 1);
         BB_PROBE(2);
         mbar_expect_tx(do_full, L::TILE);
         for (int pn = 0; pn < PANELS; ++pn)
-          tma_load_2d(smem + L::DO_OFF + pn * 16384, &tdo, do_full, h * D + pn * 64, qrow0);
+          if (!MC)
+            tma_load_2d(smem + L::DO_OFF + pn * 16384, &tdo, do_full, h * D + pn * 64, qrow0);
+          else if (crank == 0)
+            tma_load_2d_mc(smem + L::DO_OFF + pn * 16384, &tdo, do_full, h * D + pn * 64, qrow0, 3);
       }
     }
   } else if (warp == 1) {
@@ -283,7 +326,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           const uint32_t a_tmem = tmem + COL_S + (ks >> 1) * 32 + (ks & 1) * 8;  // P of q chunk c in its own S columns
           umma_ts(tmem + COL_DV, a_tmem, sw128_desc(do_base + ks * 2048, 16384, 1024), idesc_acc, (it | ks) != 0);
         }
-        umma_commit(do_empty);  // dP(t) and dV(t) have read dO(t)
+        if (MC)
+          umma_commit_mc(do_empty, 3);  // dP(t) and dV(t) have read dO(t) (both CTAs count)
+        else
+          umma_commit(do_empty);
       }
       __syncwarp();
       if (wn < n_work) {
@@ -301,7 +347,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           const uint64_t ad = sw128_desc(ds_base + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024);
           umma_ss(tmem + COL_DK, ad, sw128_desc(q_base + ks * 2048, 16384, 1024), idesc_acc, (it | ks) != 0);
         }
-        umma_commit(&q_empty[qs]);
+        if (MC)
+          umma_commit_mc(&q_empty[qs], 3);
+        else
+          umma_commit(&q_empty[qs]);
 #if BB_BWD_DQ128
         // one N=D MMA group (N=64 instructions are issue-bound at ~48 clk vs 32 nominal,
         // tools/ubench_mma_rate.cu); both halves become ready together
@@ -554,7 +603,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (MC)
+    cluster_sync();  // no CTA leaves while its partner may still multicast into it
+  else
+    __syncthreads();
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
@@ -597,8 +649,26 @@ int launch_bwd_d(const bb_attn_bwd_args& a, cudaStream_t st) {
       return BB_ERR_CUDA;
     attr_done |= uint64_t(1) << dev;
   }
-  dim3 grid(static_cast<unsigned>((a.n_k + 127) / 128), a.hkv);
-  kern<<<grid, BWD_THREADS, BwdSmem<D>::BYTES, st>>>(tq, tk, tv, tdo, tdq, p);
+  const unsigned n_kt = static_cast<unsigned>((a.n_k + 127) / 128);
+  if (MC) {  // clusters of two adjacent key tiles (an odd count gets an empty partner)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((n_kt + 1) & ~1u, a.hkv);
+    cfg.blockDim = dim3(BWD_THREADS);
+    cfg.dynamicSmemBytes = BwdSmem<D>::BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (check_cuda(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tdo, tdq, p), "attn_bwd cluster launch"))
+      return BB_ERR_CUDA;
+  } else {
+    dim3 grid(n_kt, a.hkv);
+    kern<<<grid, BWD_THREADS, BwdSmem<D>::BYTES, st>>>(tq, tk, tv, tdo, tdq, p);
+  }
   return check_launch("attn_bwd_kernel");
 }
 
