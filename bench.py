@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--layout", default="zigzag")
     ap.add_argument("--backward", default="burst_backward", choices=["burst_backward", "ring_backward"])
     ap.add_argument("--topology", default=None, help="RxM two-level ring, e.g. 2x4 (default 1xN)")
+    ap.add_argument("--transport", default="ce", choices=["ce", "collective"],
+                    help="ring exchange: copy-engine pushes into IPC arenas (ce) or NCCL send/recv (collective)")
+    ap.add_argument("--slots", type=int, default=None, help="ce transport: arena slots per channel (default N-1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -231,6 +234,7 @@ def workload_config(args, world: int) -> dict:
         "layout": args.layout,
         "backward": args.backward,
         "parallelism": f"context-parallel ring x{world}",
+        "ring_transport": (args.transport if world > 1 else None),
         "l2": "inputs larger than L2 (Q,K,V,dO shards >= 126 MB each at N<=8)",
     }
 
@@ -264,7 +268,7 @@ def run_gpu(args) -> None:
     layout = ShardLayout(args.layout, args.seq, world, args.block_len if args.layout == "block_striped" else None)
     mask = make_mask(args)
     topo = Topology(*map(int, args.topology.split("x"))) if args.topology else None
-    ring = ProcessRing(layout, mask, topo, head_dim=d)
+    ring = ProcessRing(layout, mask, topo, head_dim=d, transport=args.transport if world > 1 else None, slots=args.slots)
     n = layout.shard_size
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
 
@@ -358,9 +362,14 @@ def run_gpu(args) -> None:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
         step_s, comp_s, comm_s, exposed = (float(x) for x in vals)
         overlap = {
+            "transport": ring.transport,
             "step_ms": step_s * 1e3, "compute_ms": comp_s * 1e3, "comm_alone_ms": comm_s * 1e3,
             "exposed_comm_ms": exposed * 1e3,
             "hidden_frac": (1.0 - min(exposed, comm_s) / comm_s) if comm_s > 0 else None,
+            # bytes this rank pushed per step / the exchange timed alone (max over ranks): the
+            # per-direction NVLink rate the ring achieves, vs 900 GB/s per direction per GPU
+            "nvlink_gbs_per_direction": ring_bytes / comm_s / 1e9 if comm_s > 0 else None,
+            "nvlink_peak_gbs_per_direction": 900.0,
             "how": "max over ranks; compute = CUDA events around each attention kernel; comm alone = same ring with kernels off",
         }
 

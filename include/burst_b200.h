@@ -174,6 +174,25 @@ int bb_lmhead_fused(const bb_lmhead_args* args, void* stream);
 int bb_gemm_bf16(const void* a, const void* b, float* c, int64_t m, int64_t n, int64_t k,
                  int32_t a_mn, int32_t b_mn, int32_t accumulate, void* stream);
 
+/* ---- Peer fabric for the one-process-per-GPU ring (csrc/bb_fabric.cu) ----
+ * Replaces the reference's payload "send" of a ring step (TransferStep /
+ * MessageLog, fabric.py:180-226; distributed.py:176-177, 283-286) with a
+ * copy-engine push over NVLink into the receiver's arena plus a stream-ordered
+ * flag.  An arena is one cudaMalloc (zero-filled) exported by CUDA IPC; peers
+ * open it once.  bb_copy_async is a D2D cudaMemcpyAsync (peer pointers go over
+ * NVLink on the copy engines, no SM work).  bb_flag_write stores `value` to a
+ * 32-bit word (local or peer) after all earlier work of `stream`;
+ * bb_flag_wait blocks `stream` until the local word is >= value. */
+int32_t bb_ipc_handle_bytes(void);
+int bb_arena_alloc(int64_t bytes, void** ptr_out);
+int bb_arena_free(void* ptr);
+int bb_ipc_export(const void* ptr, void* handle_out);
+int bb_ipc_import(const void* handle, void** ptr_out);
+int bb_ipc_close(void* ptr);
+int bb_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+int bb_flag_write(void* flag, uint32_t value, void* stream);
+int bb_flag_wait(const void* flag, uint32_t value, void* stream);
+
 const char* bb_last_error(void);
 /* Diagnostics: with BB_PROBE=1 in the environment, kernels record per-phase
  * clock64() stamps of CTA (0,0) for its first tiles; copies n int64 to host. */

@@ -29,6 +29,15 @@ EXPORTS = (
     "bb_lmhead_workspace_bytes",
     "bb_lmhead_fused",
     "bb_gemm_bf16",
+    "bb_ipc_handle_bytes",
+    "bb_arena_alloc",
+    "bb_arena_free",
+    "bb_ipc_export",
+    "bb_ipc_import",
+    "bb_ipc_close",
+    "bb_copy_async",
+    "bb_flag_write",
+    "bb_flag_wait",
     "bb_last_error",
     "bb_debug_probe",
     "bb_abi_version",
@@ -140,12 +149,21 @@ def load(path: os.PathLike | str | None = None) -> C.CDLL:
     lib.bb_lmhead_workspace_bytes.restype = i64
     lib.bb_lmhead_fused.argtypes = [C.POINTER(BbLmheadArgs), vp]
     lib.bb_gemm_bf16.argtypes = [vp, vp, vp, i64, i64, i64, i32, i32, i32, vp]
+    lib.bb_ipc_handle_bytes.restype = i32
+    lib.bb_arena_alloc.argtypes = [i64, C.POINTER(vp)]
+    lib.bb_arena_free.argtypes = [vp]
+    lib.bb_ipc_export.argtypes = [vp, vp]
+    lib.bb_ipc_import.argtypes = [vp, C.POINTER(vp)]
+    lib.bb_ipc_close.argtypes = [vp]
+    lib.bb_copy_async.argtypes = [vp, vp, i64, vp]
+    lib.bb_flag_write.argtypes = [vp, C.c_uint32, vp]
+    lib.bb_flag_wait.argtypes = [vp, C.c_uint32, vp]
     lib.bb_last_error.restype = C.c_char_p
     lib.bb_debug_probe.argtypes = [vp, i32]
     lib.bb_abi_version.restype = i32
     lib.bb_launch_count.restype = i64
     for name in EXPORTS:
-        if name not in ("bb_lmhead_workspace_bytes", "bb_last_error", "bb_abi_version", "bb_launch_count"):
+        if name not in ("bb_lmhead_workspace_bytes", "bb_ipc_handle_bytes", "bb_last_error", "bb_abi_version", "bb_launch_count"):
             getattr(lib, name).restype = C.c_int
     if path is None:
         _lib = lib

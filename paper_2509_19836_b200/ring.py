@@ -9,11 +9,19 @@ is exactly the reference's payloads (distributed.py:64-101):
   burst backward Q_j, dO_j, D_j, lse_j  +  dQ_j partial  (QPayload)
   ring backward  K_j, V_j               +  dK_j/dV_j partials (KvPayload + grads)
 
-Overlap: the read-only part of step t+1's payload is posted
-(NCCL send/recv on NCCL's stream) before step t's kernel is launched, so the
-transfer runs under the compute; gradient partials are produced into a fresh
-buffer by step t's kernel and sent straight to their owner afterwards (delayed
-gradient send) while step t+1 computes.  Own shard is computed first, so a
+Two transports carry the payloads:
+
+* ``"ce"`` (default on GPUs): copy-engine pushes over NVLink into CUDA-IPC
+  arenas with stream-ordered flags (``peer.Channel``).  Every read-only payload
+  of the pass is pushed at pass start on a copy stream, the consumer stream
+  waits on a local flag right before the kernel that reads it, and gradient
+  partials are pushed to their owner as soon as the kernel producing them ends
+  (delayed gradient send).  No SM is used by the exchange, so the
+  attention kernels, which hold every SM, never delay it.
+* ``"collective"``: torch.distributed P2P (NCCL on GPUs, gloo for the CPU tests):
+  the read-only part of step t+1's payload is posted before step t's kernel
+  is launched; gradient partials are sent after the kernel.
+  Own shard is computed first, so a
 pass needs G-1 read-only hops (the reference's MessageLog still counts G).
 The visit order follows ``build_ring_plan``: flat (1xG) receives from the ring
 predecessor; a two-level plan (e.g. 2x4) orders shards node-major with intra
@@ -53,7 +61,8 @@ class RingStats:
 class ProcessRing:
     """Ring attention for one rank: ``forward`` -> (O, lse); ``backward`` -> (dQ, dK, dV)."""
 
-    def __init__(self, layout: ShardLayout, mask: MaskSpec, topology: Topology | None = None, group=None, head_dim: int | None = None):
+    def __init__(self, layout: ShardLayout, mask: MaskSpec, topology: Topology | None = None, group=None,
+                 head_dim: int | None = None, transport: str | None = None, slots: int | None = None):
         self.layout = layout
         self.mask = mask
         validate_mask(mask, layout.seq_len)
@@ -73,6 +82,20 @@ class ProcessRing:
         self.stats = RingStats()
         self.compute = True  # False: run only the exchanges (communication-alone timing)
         self.record = False  # True: CUDA events around every kernel launch (compute-lane time)
+        if transport is None:
+            transport = "ce" if self.device.type == "cuda" and self.world > 1 else "collective"
+        if transport not in ("ce", "collective"):
+            raise ValueError(f"unknown ring transport {transport!r} (expected 'ce' or 'collective')")
+        if transport == "ce" and self.device.type != "cuda":
+            raise ValueError("the copy-engine transport needs CUDA devices")
+        self.transport = transport
+        self.slots = slots  # arena slots per channel (default world-1: every payload of a pass in flight)
+        self._channels: dict = {}
+        self._parts: dict = {}  # per gradient channel: two local partial buffers (double-buffered)
+        self._xs_data = self._xs_grad = None
+        # step s (1..G-1): rank whose shard I hold / rank holding mine
+        self._src = [None] + [self.order[t] for t in range(1, self.world)]
+        self._dst = [None] + [self._who_had_me(t) for t in range(1, self.world)]
 
     def _launch(self, fn, *a, **kw):
         if not self.compute:
@@ -129,6 +152,9 @@ class ProcessRing:
             return o_full, lse_full
         o = torch.zeros(n, hq, d, dtype=torch.float32, device=q.device) if o is None else o.zero_()
         lse = torch.full((hq, n), float("-inf"), device=q.device) if lse is None else lse.fill_(float("-inf"))
+        if self.transport == "ce" and self.world > 1:
+            self._forward_ce(q, k, v, o, lse, d)
+            return o, lse
         bufs = [(k, v)] + [(torch.empty_like(k), torch.empty_like(v)) for _ in range(2)]
         pending = None
         for t in range(self.world):
@@ -166,10 +192,11 @@ class ProcessRing:
         dq = torch.zeros(q.shape, dtype=torch.float32, device=q.device) if dq is None else dq.zero_()
         dk = torch.zeros(k.shape, dtype=torch.float32, device=q.device) if dk is None else dk.zero_()
         dv = torch.zeros(v.shape, dtype=torch.float32, device=q.device) if dv is None else dv.zero_()
+        ce = self.transport == "ce" and self.world > 1
         if kind == BURST_BACKWARD:
-            self._burst(q, k, v, do, lse, delta, dq, dk, dv, d)
+            (self._burst_ce if ce else self._burst)(q, k, v, do, lse, delta, dq, dk, dv, d)
         elif kind == RING_BACKWARD:
-            self._ringbwd(q, k, v, do, lse, delta, dq, dk, dv, d)
+            (self._ringbwd_ce if ce else self._ringbwd)(q, k, v, do, lse, delta, dq, dk, dv, d)
         else:
             raise ValueError(f"unknown backward {kind!r}")
         return dq, dk, dv
@@ -264,6 +291,117 @@ class ProcessRing:
                 w.wait()
             dk.add_(grad_pending[2][0])
             dv.add_(grad_pending[2][1])
+
+    # -------------------------------------------------------------- copy-engine transport
+    def _channel(self, name: str, tensors, grad: bool):
+        """Channel ``name`` for payloads shaped like ``tensors`` (created collectively on first use).
+        Data channels carry a shard from its owner to the rank computing on it; gradient
+        channels carry the partial computed on a shard back to its owner."""
+        spec = [(tuple(t.shape), t.dtype) for t in tensors]
+        ch = self._channels.get(name)
+        if ch is None or ch.spec != spec:
+            from .peer import Channel
+
+            if ch is not None:
+                ch.close()
+            src, dst = (self._dst, self._src) if grad else (self._src, self._dst)
+            ch = Channel(name, spec, src, dst, self.rank, self.world, self.device, self.group, self.slots)
+            self._channels[name] = ch
+        return ch
+
+    def _streams(self):
+        if self._xs_data is None:
+            self._xs_data = torch.cuda.Stream(self.device)
+            self._xs_grad = torch.cuda.Stream(self.device)
+        return torch.cuda.current_stream(self.device), self._xs_data, self._xs_grad
+
+    def _push_all(self, ch, payload, cs, xs):
+        """Queue every step's push of this rank's read-only payload (copy engines, in step order)."""
+        ch.begin()
+        xs.wait_stream(cs)  # payload produced on the compute stream
+        for s in range(1, self.world):
+            ch.push(s, list(payload), xs)
+        self.stats.bytes_sent += (self.world - 1) * ch.payload_bytes
+
+    def _forward_ce(self, q, k, v, o, lse, d):
+        cs, xs, _ = self._streams()
+        ch = self._channel("kv", (k, v), grad=False)
+        self._push_all(ch, (k, v), cs, xs)
+        for t in range(self.world):
+            j = self.order[t]
+            kv = (k, v) if t == 0 else ch.wait(t, cs)
+            if self.counts[self.rank, j]:
+                self._launch(K.attn_fwd_step, q, kv[0], kv[1], o, lse, self.layout, self.dmask, self.rank + 1, j + 1,
+                             self._scale(d), n_q=q.shape[0])
+            if t > 0:
+                ch.release(t, cs)
+        cs.wait_stream(xs)
+
+    def _grad_pass(self, data_name, data, grad_name, own_acc, launch, skip):
+        """Shared CE schedule of both backward passes: ``data`` (read-only) is pushed to every rank
+        that computes on it; at step t the kernel accumulates into the own accumulators (t = 0) or a
+        fresh partial that is pushed to the shard's owner, whose compute stream adds it (lag 2)."""
+        cs, xs, xg = self._streams()
+        dch = self._channel(data_name, data, grad=False)
+        gch = self._channel(grad_name, own_acc, grad=True)
+        self._push_all(dch, data, cs, xs)
+        gch.begin()
+        parts = self._parts.get(grad_name)
+        if parts is None or [tuple(p.shape) for p in parts[0]] != [tuple(a.shape) for a in own_acc]:
+            parts = [tuple(torch.empty_like(a) for a in own_acc) for _ in range(2)]
+            self._parts[grad_name] = parts
+        part_free = [None, None]
+        lag = 2
+
+        def fold(s):  # add the partial of my shard computed elsewhere at step s
+            views = gch.wait(s, cs)
+            if self.compute:
+                for a, g in zip(own_acc, views):
+                    a.add_(g)
+            gch.release(s, cs)
+
+        for t in range(self.world):
+            j = self.order[t]
+            if t == 0:
+                payload, acc = data, own_acc
+            else:
+                payload = dch.wait(t, cs)
+                acc = parts[t % 2]
+                if part_free[t % 2] is not None:
+                    cs.wait_event(part_free[t % 2])
+                if self.compute:
+                    for a in acc:
+                        a.zero_()
+            if not skip(j):
+                self._launch(launch, payload, acc, j)
+            if t > 0:
+                dch.release(t, cs)
+                xg.wait_stream(cs)
+                gch.push(t, list(acc), xg)
+                self.stats.bytes_sent += gch.payload_bytes
+                ev = torch.cuda.Event()
+                ev.record(xg)
+                part_free[t % 2] = ev
+            if t - lag >= 1:
+                fold(t - lag)
+        for s in range(max(1, self.world - lag), self.world):
+            fold(s)
+        cs.wait_stream(xs)
+        cs.wait_stream(xg)
+
+    def _burst_ce(self, q, k, v, do, lse, delta, dq, dk, dv, d):
+        def launch(payload, acc, j):
+            K.attn_bwd_step(payload[0], k, v, payload[1], payload[2], payload[3], acc[0], dk, dv,
+                            self.layout, self.dmask, j + 1, self.rank + 1, self._scale(d))
+
+        self._grad_pass("qp", (q, do, lse, delta), "dq", (dq,), launch, lambda j: not self.counts[j, self.rank])
+
+    def _ringbwd_ce(self, q, k, v, do, lse, delta, dq, dk, dv, d):
+        def launch(payload, acc, j):
+            K.attn_bwd_step(q, payload[0], payload[1], do, lse, delta, dq, acc[0], acc[1],
+                            self.layout, self.dmask, self.rank + 1, j + 1, self._scale(d))
+
+        self._grad_pass("kv", (k, v), "dkv", (dk, dv), launch, lambda j: not self.counts[self.rank, j])
 
     def _who_had_me(self, t: int) -> int:
         """Rank that computed on MY shard at step t (it sends me that gradient partial)."""

@@ -42,27 +42,38 @@ def main():
         glob = [torch.from_numpy(rng.uniform(-1, 1, (n, h, d))).float().to(torch.bfloat16) for h in (hq, hkv, hkv, hq)]
         rows = torch.from_numpy(device_token_ids(layout, rank + 1) - 1)
         q, k, v, do = (t[rows].contiguous().to(dev) for t in glob)
-        ring = ProcessRing(layout, mask, Topology(*topo), head_dim=d)
-        o, lse = ring.forward(q, k, v)
-        dq, dk, dv = ring.backward(q, k, v, do, o, lse, kind=backward)
-        torch.cuda.synchronize()
         ref = O.mh_ring_attention(*(t.double().numpy() for t in glob), (kind, n, world, None), mt, O.ring_visit(*topo),
                                   backward="burst" if backward == "burst_backward" else "ring")
         r = rows.numpy()
-        rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
-        errs = {
-            "o": float(np.abs(o.double().cpu().numpy() - ref["o"][r]).max()),
-            "lse": float(np.abs(lse.double().cpu().numpy() - ref["lse"][:, r]).max()),
-            "dq": rel(dq.double().cpu().numpy(), ref["dq"][r]),
-            "dk": rel(dk.double().cpu().numpy(), ref["dk"][r]),
-            "dv": rel(dv.double().cpu().numpy(), ref["dv"][r]),
-        }
-        ok = errs["o"] < 1e-2 and errs["lse"] < 2e-3 and errs["dq"] < 1e-2 and errs["dk"] < 1e-2 and errs["dv"] < 1e-2
-        failures += not ok
-        print(f"rank {rank} {kind} {topo} {mname} {backward}: {'ok' if ok else 'FAIL'} {errs} sent={ring.stats.bytes_sent}", flush=True)
+        variants = [("ce", None), ("collective", None)] + ([("ce", 1)] if backward == "burst_backward" else [])
+        for transport, slots in variants:
+            ring = ProcessRing(layout, mask, Topology(*topo), head_dim=d, transport=transport, slots=slots)
+            for rep in range(2):  # later passes exercise the cross-pass slot hand-over (flag epochs)
+                o, lse = ring.forward(q, k, v)
+                dq, dk, dv = ring.backward(q, k, v, do, o, lse, kind=backward)
+            torch.cuda.synchronize()
+            failures += _report(rank, f"{kind} {topo} {mname} {backward} {transport} slots={slots}", o, lse, dq, dk, dv,
+                                ref, r, ring.stats.bytes_sent)
     dist.barrier()
     dist.destroy_process_group()
     sys.exit(1 if failures else 0)
+
+
+def _report(rank, label, o, lse, dq, dk, dv, ref, r, sent) -> int:
+    rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
+    errs = {
+        "o": float(np.abs(o.double().cpu().numpy() - ref["o"][r]).max()),
+        "lse": float(np.abs(lse.double().cpu().numpy() - ref["lse"][:, r]).max()),
+        "dq": rel(dq.double().cpu().numpy(), ref["dq"][r]),
+        "dk": rel(dk.double().cpu().numpy(), ref["dk"][r]),
+        "dv": rel(dv.double().cpu().numpy(), ref["dv"][r]),
+    }
+    ok = errs["o"] < 1e-2 and errs["lse"] < 2e-3 and errs["dq"] < 1e-2 and errs["dk"] < 1e-2 and errs["dv"] < 1e-2
+    line = f"rank {rank} {label}: {'ok' if ok else 'FAIL'} {errs} sent={sent}"
+    print(line, flush=True)
+    with open(os.path.join(os.environ.get("BB_RING_LOG_DIR", "."), f"ring_check_rank{rank}.log"), "a") as f:
+        f.write(line + "\n")
+    return int(not ok)
 
 
 if __name__ == "__main__":
