@@ -360,17 +360,21 @@ def run_gpu(args) -> None:
         ring.compute = True
         vals = torch.tensor([step_s, comp_s, comm_s, max(0.0, step_s - comp_s)], device=dev, dtype=torch.float64)
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-        step_s, comp_s, comm_s, exposed = (float(x) for x in vals)
+        step_s, comp_s, comm_s, idle = (float(x) for x in vals)
+        # exposed = step - the busiest rank's kernel time: what the exchange (and its folds) add
+        # to the critical path.  max_rank_idle also counts ranks waiting on a busier peer.
+        exposed = max(0.0, step_s - comp_s)
         overlap = {
             "transport": ring.transport,
             "step_ms": step_s * 1e3, "compute_ms": comp_s * 1e3, "comm_alone_ms": comm_s * 1e3,
             "exposed_comm_ms": exposed * 1e3,
             "hidden_frac": (1.0 - min(exposed, comm_s) / comm_s) if comm_s > 0 else None,
+            "max_rank_idle_ms": idle * 1e3,
             # bytes this rank pushed per step / the exchange timed alone (max over ranks): the
             # per-direction NVLink rate the ring achieves, vs 900 GB/s per direction per GPU
             "nvlink_gbs_per_direction": ring_bytes / comm_s / 1e9 if comm_s > 0 else None,
             "nvlink_peak_gbs_per_direction": 900.0,
-            "how": "max over ranks; compute = CUDA events around each attention kernel; comm alone = same ring with kernels off",
+            "how": "max over ranks; compute = CUDA events around each attention kernel (busiest rank); comm alone = same ring with kernels off; exposed = step - compute",
         }
 
     # ---- e2e through the public API with pinned host buffers.  Every step copies its

@@ -120,6 +120,11 @@ typedef struct bb_attn_bwd_args {
   int32_t k_device;
   bb_layout layout;
   bb_mask mask;
+  /* kv heads [kv_head_begin, kv_head_end) only (their q heads, dK/dV rows and dQ
+   * columns); kv_head_end == 0 means all hkv heads.  Lets the ring split a step's
+   * work so a gradient transfer can overlap the other half. */
+  int32_t kv_head_begin;
+  int32_t kv_head_end;
 } bb_attn_bwd_args;
 
 int bb_attn_fwd_step(const bb_attn_fwd_args* args, void* stream);

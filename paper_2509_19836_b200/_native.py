@@ -103,6 +103,8 @@ class BbAttnBwdArgs(C.Structure):
         ("k_device", C.c_int32),
         ("layout", BbLayout),
         ("mask", BbMask),
+        ("kv_head_begin", C.c_int32),
+        ("kv_head_end", C.c_int32),
     ]
 
 

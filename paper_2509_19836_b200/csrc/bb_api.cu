@@ -160,6 +160,9 @@ int bb_attn_bwd_step(const bb_attn_bwd_args* a, void* stream) {
   if (int rc = validate_ring_step(a->layout, a->mask, a->n_q, a->n_k, a->hq, a->hkv, a->head_dim, a->q_device,
                                   a->k_device, "bb_attn_bwd_step"))
     return rc;
+  if (a->kv_head_end != 0 && (a->kv_head_begin < 0 || a->kv_head_end > a->hkv || a->kv_head_begin >= a->kv_head_end))
+    return set_error(BB_ERR_INVALID, "bb_attn_bwd_step: kv head range [%d, %d) outside [0, %d)", a->kv_head_begin,
+                     a->kv_head_end, a->hkv);
   return launch_attn_bwd(*a, static_cast<cudaStream_t>(stream));
 }
 

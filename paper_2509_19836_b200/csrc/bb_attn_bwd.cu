@@ -40,7 +40,7 @@ namespace {
 #endif
 constexpr int NG = BB_BWD_NG;
 #ifndef BB_BWD_MC
-#define BB_BWD_MC 1
+#define BB_BWD_MC 0  // 2-CTA multicast clusters: +1 % but hang intermittently at small shards (tools/bwd_heads_check.py)
 #endif
 constexpr bool MC = BB_BWD_MC;
 #ifndef BB_BWD_DQ128
@@ -76,6 +76,7 @@ struct BwdParams {
   float* dv;
   int64_t n_q, n_k;
   int32_t hq, hkv;
+  int32_t kv_head0;  // first kv head of this launch (grid.y covers the range)
   float scale, scale_log2;
   int32_t q_device, k_device;
   LayoutD layout;
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
   float* vec_s = reinterpret_cast<float*>(smem + L::VEC_OFF);
 
-  const int kv_head = blockIdx.y;
+  const int kv_head = p.kv_head0 + static_cast<int>(blockIdx.y);
   const int group = p.hq / p.hkv;
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 128;  // low key tiles carry the most work
   // MC: clusters of two adjacent key tiles share every Q / dO tile through a TMA multicast
@@ -632,6 +633,8 @@ int launch_bwd_d(const bb_attn_bwd_args& a, cudaStream_t st) {
   p.n_k = a.n_k;
   p.hq = a.hq;
   p.hkv = a.hkv;
+  p.kv_head0 = a.kv_head_begin;
+  const unsigned n_heads = static_cast<unsigned>((a.kv_head_end ? a.kv_head_end : a.hkv) - a.kv_head_begin);
   p.scale = a.softmax_scale;
   p.scale_log2 = a.softmax_scale * 1.4426950408889634f;
   p.q_device = a.q_device;
@@ -652,7 +655,7 @@ int launch_bwd_d(const bb_attn_bwd_args& a, cudaStream_t st) {
   const unsigned n_kt = static_cast<unsigned>((a.n_k + 127) / 128);
   if (MC) {  // clusters of two adjacent key tiles (an odd count gets an empty partner)
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((n_kt + 1) & ~1u, a.hkv);
+    cfg.gridDim = dim3((n_kt + 1) & ~1u, n_heads);
     cfg.blockDim = dim3(BWD_THREADS);
     cfg.dynamicSmemBytes = BwdSmem<D>::BYTES;
     cfg.stream = st;
@@ -666,7 +669,7 @@ int launch_bwd_d(const bb_attn_bwd_args& a, cudaStream_t st) {
     if (check_cuda(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tdo, tdq, p), "attn_bwd cluster launch"))
       return BB_ERR_CUDA;
   } else {
-    dim3 grid(n_kt, a.hkv);
+    dim3 grid(n_kt, n_heads);
     kern<<<grid, BWD_THREADS, BwdSmem<D>::BYTES, st>>>(tq, tk, tv, tdo, tdq, p);
   }
   return check_launch("attn_bwd_kernel");

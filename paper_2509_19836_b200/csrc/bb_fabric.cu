@@ -65,8 +65,16 @@ int bb_arena_alloc(int64_t bytes, void** ptr_out) {
   *ptr_out = nullptr;
   void* p = nullptr;
   if (int rc = check_cuda(cudaMalloc(&p, static_cast<size_t>(bytes)), "cudaMalloc(arena)")) return rc;
-  // flags start at epoch 0 (nothing ready / nothing released)
-  if (int rc = check_cuda(cudaMemset(p, 0, static_cast<size_t>(bytes)), "cudaMemset(arena)")) {
+  // Flags start at epoch 0 (nothing ready / nothing released).  The zero fill runs on a
+  // private non-blocking stream and is waited for here: on the legacy stream it would queue
+  // behind the caller's in-flight ring work (which may be blocked on flags of peers) and
+  // could land after a peer's first flag write into this arena.
+  cudaStream_t z = nullptr;
+  int rc = check_cuda(cudaStreamCreateWithFlags(&z, cudaStreamNonBlocking), "cudaStreamCreate(arena)");
+  if (!rc) rc = check_cuda(cudaMemsetAsync(p, 0, static_cast<size_t>(bytes), z), "cudaMemsetAsync(arena)");
+  if (!rc) rc = check_cuda(cudaStreamSynchronize(z), "cudaStreamSynchronize(arena)");
+  if (z) cudaStreamDestroy(z);
+  if (rc) {
     cudaFree(p);
     return rc;
   }

@@ -120,8 +120,10 @@ def attn_fwd_step(
 def attn_bwd_step(
     q, k, v, dout, lse, delta, dq, dk, dv,
     layout: ShardLayout, mask: DeviceMask, q_device: int, k_device: int, softmax_scale: float,
+    kv_heads: tuple[int, int] | None = None,
 ) -> None:
-    """Accumulate one (query shard, key shard) pair into dq/dk/dv; see bb_attn_bwd_step."""
+    """Accumulate one (query shard, key shard) pair into dq/dk/dv; see bb_attn_bwd_step.
+    ``kv_heads=(b, e)`` restricts the step to kv heads [b, e) and their query heads."""
     for t, name in ((q, "Q"), (k, "K"), (v, "V"), (dout, "dO")):
         _require(t, torch.bfloat16, name)
     for t, name in ((lse, "lse"), (delta, "D"), (dq, "dQ"), (dk, "dK"), (dv, "dV")):
@@ -132,6 +134,7 @@ def attn_bwd_step(
         n_q=q.shape[0], n_k=k.shape[0], hq=q.shape[1], hkv=k.shape[1], head_dim=q.shape[2],
         softmax_scale=float(softmax_scale), q_device=q_device, k_device=k_device,
         layout=layout_struct(layout), mask=mask.struct,
+        kv_head_begin=kv_heads[0] if kv_heads else 0, kv_head_end=kv_heads[1] if kv_heads else 0,
     )
     N.check(N.load().bb_attn_bwd_step(C.byref(a), C.c_void_p(_stream(q.device))))
 

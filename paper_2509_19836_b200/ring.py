@@ -91,8 +91,9 @@ class ProcessRing:
         self.transport = transport
         self.slots = slots  # arena slots per channel (default world-1: every payload of a pass in flight)
         self._channels: dict = {}
-        self._parts: dict = {}  # per gradient channel: two local partial buffers (double-buffered)
-        self._xs_data = self._xs_grad = None
+        self._grad_state: dict = {}  # per gradient channel: partial buffers, their events, fold target
+        self.split_own = True  # CE backward: own step split by kv heads around the remote steps
+        self._xs_data = self._xs_grad = self._xs_fold = None
         # step s (1..G-1): rank whose shard I hold / rank holding mine
         self._src = [None] + [self.order[t] for t in range(1, self.world)]
         self._dst = [None] + [self._who_had_me(t) for t in range(1, self.world)]
@@ -313,6 +314,7 @@ class ProcessRing:
         if self._xs_data is None:
             self._xs_data = torch.cuda.Stream(self.device)
             self._xs_grad = torch.cuda.Stream(self.device)
+            self._xs_fold = torch.cuda.Stream(self.device, priority=-1)  # folds win the next free SM
         return torch.cuda.current_stream(self.device), self._xs_data, self._xs_grad
 
     def _push_all(self, ch, payload, cs, xs):
@@ -337,71 +339,96 @@ class ProcessRing:
                 ch.release(t, cs)
         cs.wait_stream(xs)
 
-    def _grad_pass(self, data_name, data, grad_name, own_acc, launch, skip):
-        """Shared CE schedule of both backward passes: ``data`` (read-only) is pushed to every rank
-        that computes on it; at step t the kernel accumulates into the own accumulators (t = 0) or a
-        fresh partial that is pushed to the shard's owner, whose compute stream adds it (lag 2)."""
+    def _grad_pass(self, data_name, data, grad_name, own_acc, launch, skip, hkv):
+        """Shared copy-engine schedule of both backward passes.
+
+        ``data`` (read-only) is pushed at pass start to every rank that computes on it.  The
+        own shard's step is split by kv heads into halves A and B: A runs first, B last.  At
+        remote step t the kernel accumulates into a zeroed partial that is pushed to the
+        shard's owner as soon as the kernel ends (and re-zeroed on the copy stream behind
+        the push).  The owner folds arriving partials into its accumulators on a
+        high-priority side stream: everything before B starts, then the last partial's
+        A heads while B runs; only the last partial's B heads are added after B."""
         cs, xs, xg = self._streams()
+        xf = self._xs_fold
         dch = self._channel(data_name, data, grad=False)
         gch = self._channel(grad_name, own_acc, grad=True)
         self._push_all(dch, data, cs, xs)
         gch.begin()
-        parts = self._parts.get(grad_name)
-        if parts is None or [tuple(p.shape) for p in parts[0]] != [tuple(a.shape) for a in own_acc]:
-            parts = [tuple(torch.empty_like(a) for a in own_acc) for _ in range(2)]
-            self._parts[grad_name] = parts
-        part_free = [None, None]
-        lag = 2
-
-        def fold(s):  # add the partial of my shard computed elsewhere at step s
-            views = gch.wait(s, cs)
-            if self.compute:
-                for a, g in zip(own_acc, views):
-                    a.add_(g)
-            gch.release(s, cs)
-
-        for t in range(self.world):
+        st = self._grad_state.get(grad_name)
+        if st is None or [tuple(p.shape) for p in st["parts"][0]] != [tuple(a.shape) for a in own_acc]:
+            st = {"parts": [tuple(torch.zeros_like(a) for a in own_acc) for _ in range(2)], "free": [None, None]}
+            self._grad_state[grad_name] = st
+        parts, free = st["parts"], st["free"]  # free[i]: partial buffer i pushed and re-zeroed
+        split = self.split_own and hkv >= 2
+        hs = [(hkv // 2) * (a.shape[1] // hkv) for a in own_acc]  # first head of half B, per accumulator
+        me, last = self.rank, self.world - 1
+        if not skip(me):
+            self._launch(launch, data, own_acc, me, (0, hkv // 2) if split else None)
+        xf.wait_stream(cs)
+        b_ready = None
+        for t in range(1, self.world):
             j = self.order[t]
-            if t == 0:
-                payload, acc = data, own_acc
-            else:
-                payload = dch.wait(t, cs)
-                acc = parts[t % 2]
-                if part_free[t % 2] is not None:
-                    cs.wait_event(part_free[t % 2])
-                if self.compute:
-                    for a in acc:
-                        a.zero_()
+            payload = dch.wait(t, cs)
+            acc = parts[t % 2]
+            if free[t % 2] is not None:
+                cs.wait_event(free[t % 2])
             if not skip(j):
-                self._launch(launch, payload, acc, j)
-            if t > 0:
-                dch.release(t, cs)
-                xg.wait_stream(cs)
-                gch.push(t, list(acc), xg)
-                self.stats.bytes_sent += gch.payload_bytes
-                ev = torch.cuda.Event()
-                ev.record(xg)
-                part_free[t % 2] = ev
-            if t - lag >= 1:
-                fold(t - lag)
-        for s in range(max(1, self.world - lag), self.world):
-            fold(s)
+                self._launch(launch, payload, acc, j, None)
+            dch.release(t, cs)
+            xg.wait_stream(cs)
+            gch.push(t, list(acc), xg)
+            self.stats.bytes_sent += gch.payload_bytes
+            if self.compute:
+                with torch.cuda.stream(xg):
+                    for x in acc:
+                        x.zero_()
+            ev = torch.cuda.Event()
+            ev.record(xg)
+            free[t % 2] = ev
+            if t == last and split:
+                b_ready = torch.cuda.Event()
+                b_ready.record(xf)  # every earlier fold (all heads) is done
+            views = gch.wait(t, xf)  # the partial of MY shard computed elsewhere at step t
+            if self.compute:
+                with torch.cuda.stream(xf):
+                    for x, g, h in zip(own_acc, views, hs):
+                        if t == last and split:
+                            x[:, :h].add_(g[:, :h])  # half B is being written by the own kernel
+                        else:
+                            x.add_(g)
+            if not (t == last and split):
+                gch.release(t, xf)
+        if split:
+            if b_ready is not None:
+                cs.wait_event(b_ready)
+            if not skip(me):
+                self._launch(launch, data, own_acc, me, (hkv // 2, hkv))
+            cs.wait_stream(xf)
+            if last >= 1:
+                views = gch.views(last)
+                if self.compute:
+                    for x, g, h in zip(own_acc, views, hs):
+                        x[:, h:].add_(g[:, h:])
+                gch.release(last, cs)
+        cs.wait_stream(xf)
         cs.wait_stream(xs)
         cs.wait_stream(xg)
 
     def _burst_ce(self, q, k, v, do, lse, delta, dq, dk, dv, d):
-        def launch(payload, acc, j):
+        def launch(payload, acc, j, heads):
             K.attn_bwd_step(payload[0], k, v, payload[1], payload[2], payload[3], acc[0], dk, dv,
-                            self.layout, self.dmask, j + 1, self.rank + 1, self._scale(d))
+                            self.layout, self.dmask, j + 1, self.rank + 1, self._scale(d), kv_heads=heads)
 
-        self._grad_pass("qp", (q, do, lse, delta), "dq", (dq,), launch, lambda j: not self.counts[j, self.rank])
+        self._grad_pass("qp", (q, do, lse, delta), "dq", (dq,), launch, lambda j: not self.counts[j, self.rank],
+                        k.shape[1])
 
     def _ringbwd_ce(self, q, k, v, do, lse, delta, dq, dk, dv, d):
-        def launch(payload, acc, j):
+        def launch(payload, acc, j, heads):
             K.attn_bwd_step(q, payload[0], payload[1], do, lse, delta, dq, acc[0], acc[1],
-                            self.layout, self.dmask, self.rank + 1, j + 1, self._scale(d))
+                            self.layout, self.dmask, self.rank + 1, j + 1, self._scale(d), kv_heads=heads)
 
-        self._grad_pass("kv", (k, v), "dkv", (dk, dv), launch, lambda j: not self.counts[self.rank, j])
+        self._grad_pass("kv", (k, v), "dkv", (dk, dv), launch, lambda j: not self.counts[self.rank, j], k.shape[1])
 
     def _who_had_me(self, t: int) -> int:
         """Rank that computed on MY shard at step t (it sends me that gradient partial)."""

@@ -170,3 +170,18 @@ def test_lmhead_matches_torch(cuda, n, vocab, dim, rows_tile):
     assert (loss - ref).abs().max().item() < 2e-3
     for got, want in ((dh, hf.grad), (dw, wf.grad)):
         assert (got - want).norm().item() / want.norm().item() < 1e-2
+
+
+def test_bwd_kv_head_halves_equal_full_step():
+    """bb_attn_bwd_step over kv-head ranges (the ring's split own step) sums to the full step for
+    every (i, j) of a 4-way zigzag causal ring with GQA; run in a subprocess under a timeout so a
+    kernel hang (seen with the 2-CTA multicast variant) fails instead of stalling the suite."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    res = subprocess.run([sys.executable, str(root / "tools" / "bwd_heads_check.py")], capture_output=True, text=True,
+                         timeout=300, env=dict(os.environ, PYTHONPATH=str(root)))
+    assert res.returncode == 0 and "OK" in res.stdout, res.stdout[-2000:] + res.stderr[-2000:]
