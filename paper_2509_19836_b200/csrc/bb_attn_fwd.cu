@@ -53,6 +53,14 @@ constexpr float RESCALE_THRESHOLD = 8.0f;
 #ifndef BB_PACK_INT
 #define BB_PACK_INT 0
 #endif
+#ifndef BB_FWD_CHUNKED
+// S read from TMEM in 32-column chunks twice (row max, then exp) instead of held whole in
+// registers: s[128] per thread spilled ~230 B to local memory at the 168-register budget.
+#define BB_FWD_CHUNKED 0  // measured 10 % slower (1162 -> 1050 TF/s full 32K): the second TMEM pass costs more than the spills
+#endif
+#ifndef BB_FWD_PINGPONG
+#define BB_FWD_PINGPONG 0  // softmax warpgroups take turns on MUFU (named barriers 1, 2): measured 16 % slower (1159 -> 972 TF/s full 32K)
+#endif
 constexpr int POLY_EVERY = BB_POLY_EVERY;  // every POLY_EVERY-th P column uses ex2_poly (>8: never)  // log2 units: P may reach 2^8 before O is rescaled
 
 template <int D>
@@ -286,9 +294,20 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 
     float m_run = -INFINITY, l_run = 0.f;
     uint32_t t = 0;
+#if BB_FWD_PINGPONG
+    // Exp passes of the two query tiles alternate on MUFU (16 lanes/clk/SM: one 128x128 pass
+    // needs all of it for 1024 cycles).  Left to themselves the two warpgroups drift into phase
+    // and each pass takes twice as long, lengthening the chain softmax(j) -> P.V(j) -> S(j+1).
+    // Only key tiles both query tiles use take turns; order per such tile: tile 0, then 1.
+    uint32_t n_both = 0, k_both = 0;
+    for (int64_t jj = j_lo; jj < j_hi; ++jj) n_both += (tile_nib(jj) & 3u) != 0 && (tile_nib(jj) >> 2) != 0;
+#endif
     for (int64_t j = j_lo; j < j_hi; ++j) {
       const int32_t cls = tile_cls(q, j);
       if (cls == TILE_SKIP) continue;
+#if BB_FWD_PINGPONG
+      const bool both = tile_cls(q ^ 1, j) != TILE_SKIP;
+#endif
       if (row == 0) FWD_PROBE(t, 16 + 8 * q);
       mbar_wait(&s_full[q], t & 1);
       if (row == 0) FWD_PROBE(t, 17 + 8 * q);
@@ -297,6 +316,40 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       if (cls == TILE_PARTIAL)
         bits = row_mask_bits(p.layout, p.mask, q_id, row_ok, p.k_device, j * 128, p.n_k, true);
       if (row == 0) FWD_PROBE(t, 22 + 8 * q);
+#if BB_FWD_CHUNKED
+      const uint32_t s_col = tmem + t_lane + q * 128u;
+      float ca[32], cb[32];
+      auto mask_chunk = [&](float(&x)[32], int c0) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          if (!mask_bit(bits, c0 + c)) x[c] = -INFINITY;
+      };
+      // pass 1: row max, two 32-column loads in flight, 3-input-max tree per chunk
+      float mx8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        tmem_ld32(s_col + half * 64, ca);
+        tmem_ld32(s_col + half * 64 + 32, cb);
+        tmem_ld_wait();
+        reg_fence(ca);
+        reg_fence(cb);
+        if (cls == TILE_PARTIAL) {
+          mask_chunk(ca, half * 64);
+          mask_chunk(cb, half * 64 + 32);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          mx8[i] = fmax3(mx8[i], ca[i], ca[i + 8]);
+          mx8[i] = fmax3(mx8[i], ca[i + 16], ca[i + 24]);
+          mx8[i] = fmax3(mx8[i], cb[i], cb[i + 8]);
+          mx8[i] = fmax3(mx8[i], cb[i + 16], cb[i + 24]);
+        }
+      }
+      const float mx = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
+      if (row == 0) FWD_PROBE(t, 23 + 8 * q);
+#else
       float s[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
@@ -319,6 +372,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 #pragma unroll
       for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(mx8[i], s[120 + i]);
       const float mx = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
+#endif
       const float m_tile = mx * sl2;
       const bool need = m_tile > m_run + RESCALE_THRESHOLD;
       float alpha = 1.f;
@@ -352,7 +406,44 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       // cubic on the FMA pipe (never for masked tiles, whose -inf scores need MUFU's exact 0).
       // P is packed to bf16x2 and stored over the S columns it came from, 32 keys at a time.
       float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#if BB_FWD_X2
+#if BB_FWD_CHUNKED
+      // pass 2: reload S chunk by chunk (one load in flight behind the chunk being
+      // exponentiated); P chunk c lands in S columns [c/2, c/2+16), all already read.
+      float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      const float2 sl2x2 = make_float2(sl2, sl2), negm2 = make_float2(neg_m, neg_m);
+      auto exp_chunk = [&](float(&x)[32], int c0) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float2 y = __ffma2_rn(make_float2(x[2 * i], x[2 * i + 1]), sl2x2, negm2);
+          const float2 e = make_float2(ex2_approx(y.x), ex2_approx(y.y));
+          acc4[i & 3] = __fadd2_rn(acc4[i & 3], e);
+          pk[i] = pack_bf16(e.x, e.y);
+        }
+        tmem_st16(s_col + c0 / 2, pk);
+      };
+      tmem_ld32(s_col, ca);
+      tmem_ld32(s_col + 32, cb);
+      tmem_ld_wait();
+      reg_fence(ca);
+      reg_fence(cb);
+      if (cls == TILE_PARTIAL) {
+        mask_chunk(ca, 0);
+        mask_chunk(cb, 32);
+      }
+      exp_chunk(ca, 0);
+      tmem_ld32(s_col + 64, ca);
+      exp_chunk(cb, 32);
+      tmem_ld_wait();
+      reg_fence(ca);
+      tmem_ld32(s_col + 96, cb);
+      if (cls == TILE_PARTIAL) mask_chunk(ca, 64);
+      exp_chunk(ca, 64);
+      tmem_ld_wait();
+      reg_fence(cb);
+      if (cls == TILE_PARTIAL) mask_chunk(cb, 96);
+      exp_chunk(cb, 96);
+#elif BB_FWD_X2
       // packed fp32x2 arithmetic (FFMA2 for the scale, FADD2 for the row sums): half the FP32
       // issue slots of the scalar form; POLY_EVERY (in pairs) moves a share to ex2_poly2.
       float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -404,11 +495,24 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         }
       };
 #endif
+#if BB_FWD_PINGPONG
+      // tile 0 waits for tile 1's pass of the previous shared key tile; tile 1 for tile 0's
+      // pass of this one (bar.sync by the waiting warpgroup + bar.arrive by the other = 256)
+      if (both && (q == 1 || k_both > 0)) named_bar_sync(1 + q, 256);
+#endif
+#if !BB_FWD_CHUNKED
       if (cls == TILE_PARTIAL)
         exp_pass(std::true_type{});
       else
         exp_pass(std::false_type{});
-#if BB_FWD_X2
+#endif
+#if BB_FWD_PINGPONG
+      if (both) {
+        if (q == 0 || k_both + 1 < n_both) named_bar_arrive(2 - q, 256);
+        ++k_both;
+      }
+#endif
+#if BB_FWD_X2 || BB_FWD_CHUNKED
       acc8[0] = acc4[0].x;
       acc8[1] = acc4[0].y;
       acc8[2] = acc4[1].x;

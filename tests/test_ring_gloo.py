@@ -154,3 +154,57 @@ def test_process_ring_matches_oracle(case):
         assert np.max(np.abs(dk - ref["dk"][rows])) < 2e-6  # fp32 accumulators (the product allocates O, lse, dQ, dK, dV in fp32)
         assert np.max(np.abs(dv - ref["dv"][rows])) < 2e-6  # fp32 accumulators (the product allocates O, lse, dQ, dK, dV in fp32)
         assert sent > 0  # own shard first: G-1 read-only hops per pass plus gradient partials
+
+
+def _autograd_worker(rank, world, port, policy_frac, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2509_19836_b200 import masks as M
+        from paper_2509_19836_b200 import ring as R
+        from paper_2509_19836_b200.autograd import burst_attention
+        from paper_2509_19836_b200.checkpointing import CheckpointPolicy
+        from paper_2509_19836_b200.fabric import Topology
+        from paper_2509_19836_b200.partitioning import ShardLayout, device_token_ids
+
+        n, hq, hkv, d = 32, 2, 1, 8
+        layout = ShardLayout("zigzag", n, world)
+        R.K = FakeKernels(layout, ("causal", None, None, None))
+        rng = np.random.default_rng(0)
+        q, k, v, do = (torch.from_numpy(rng.uniform(-1, 1, (n, h, d))) for h in (hq, hkv, hkv, hq))
+        rows = torch.from_numpy(device_token_ids(layout, rank + 1) - 1)
+        ql, kl, vl = (t[rows].contiguous().requires_grad_() for t in (q, k, v))
+        ring = R.ProcessRing(layout, M.causal_mask(), Topology(1, world), head_dim=d)
+        policy = CheckpointPolicy("sequence_selective", policy_frac) if policy_frac is not None else None
+        o = burst_attention(ql, kl, vl, ring, "burst_backward", policy)
+        (o.double() * do[rows]).sum().backward()
+        out_q.put((rank, rows.numpy(), o.detach().numpy(), ql.grad.numpy(), kl.grad.numpy(), vl.grad.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("policy_frac", [None, 0.5])
+def test_autograd_function_matches_oracle(policy_frac):
+    """BurstAttention.apply over a 2-rank gloo ring: O and the autograd gradients equal the
+    oracle; with a sequence_selective policy the dropped (O, lse) prefix is recomputed."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    out_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_autograd_worker, args=(r, world, port, policy_frac, out_q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [out_q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n, hq, hkv, d = 32, 2, 1, 8
+    rng = np.random.default_rng(0)
+    q, k, v, do = (rng.uniform(-1, 1, (n, h, d)) for h in (hq, hkv, hkv, hq))
+    ref = O.mh_ring_attention(q, k, v, do, ("zigzag", n, world, None), ("causal", None, None, None),
+                              O.ring_visit(1, world), backward="burst")
+    for rank, rows, o, dq, dk, dv in res:
+        assert np.max(np.abs(o - ref["o"][rows])) < 2e-6
+        assert np.max(np.abs(dq - ref["dq"][rows])) < 2e-6
+        assert np.max(np.abs(dk - ref["dk"][rows])) < 2e-6
+        assert np.max(np.abs(dv - ref["dv"][rows])) < 2e-6

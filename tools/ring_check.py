@@ -46,11 +46,24 @@ def main():
                                   backward="burst" if backward == "burst_backward" else "ring")
         r = rows.numpy()
         variants = [("ce", None), ("collective", None)] + ([("ce", 1)] if backward == "burst_backward" else [])
+        if backward == "burst_backward" and topo[0] == 1:
+            variants.append(("autograd", None))
         for transport, slots in variants:
-            ring = ProcessRing(layout, mask, Topology(*topo), head_dim=d, transport=transport, slots=slots)
-            for rep in range(2):  # later passes exercise the cross-pass slot hand-over (flag epochs)
-                o, lse = ring.forward(q, k, v)
-                dq, dk, dv = ring.backward(q, k, v, do, o, lse, kind=backward)
+            if transport == "autograd":  # BurstAttention.apply (CE ring) with sequence-selective recompute
+                from paper_2509_19836_b200.autograd import BurstAttention
+                from paper_2509_19836_b200.checkpointing import CheckpointPolicy
+
+                ring = ProcessRing(layout, mask, Topology(*topo), head_dim=d)
+                ql, kl, vl = (t.clone().requires_grad_() for t in (q, k, v))
+                o, lse = BurstAttention.apply(ql, kl, vl, ring, backward, CheckpointPolicy("sequence_selective", 0.5))
+                (o * do.float()).sum().backward()
+                dq, dk, dv = ql.grad.float(), kl.grad.float(), vl.grad.float()
+                o, lse = o.detach(), lse.detach()
+            else:
+                ring = ProcessRing(layout, mask, Topology(*topo), head_dim=d, transport=transport, slots=slots)
+                for rep in range(2):  # later passes exercise the cross-pass slot hand-over (flag epochs)
+                    o, lse = ring.forward(q, k, v)
+                    dq, dk, dv = ring.backward(q, k, v, do, o, lse, kind=backward)
             torch.cuda.synchronize()
             failures += _report(rank, f"{kind} {topo} {mname} {backward} {transport} slots={slots}", o, lse, dq, dk, dv,
                                 ref, r, ring.stats.bytes_sent)
