@@ -54,6 +54,11 @@ def _check(rc: int) -> None:
     N.check(rc)
 
 
+def _arena_tensor(ptr: int, nbytes: int, device: torch.device) -> torch.Tensor:
+    """uint8 tensor over an arena's device bytes (no copy, not owned by torch)."""
+    return torch.as_tensor(_DeviceBytes(ptr, nbytes), device=device)
+
+
 class Channel:
     """One payload kind flowing between ring ranks through copy-engine pushes (see module doc)."""
 
@@ -94,7 +99,7 @@ class Channel:
             _check(lib.bb_ipc_import(C.create_string_buffer(handles[r], hbytes), C.byref(q)))
             self.peer_base[r] = int(q.value)
         self._lib = lib
-        self.arena = torch.as_tensor(_DeviceBytes(self.base, total), device=device)
+        self.arena = _arena_tensor(self.base, total, device)
         self.epoch = 0
         self.bytes_pushed = 0
 
