@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--transport", default="ce", choices=["ce", "collective"],
                     help="ring exchange: copy-engine pushes into IPC arenas (ce) or NCCL send/recv (collective)")
     ap.add_argument("--slots", type=int, default=None, help="ce transport: arena slots per channel (default N-1)")
+    ap.add_argument("--ce-fanout", type=int, default=None, help="ce transport: copy streams per push (default BB_CE_FANOUT or 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -268,7 +269,8 @@ def run_gpu(args) -> None:
     layout = ShardLayout(args.layout, args.seq, world, args.block_len if args.layout == "block_striped" else None)
     mask = make_mask(args)
     topo = Topology(*map(int, args.topology.split("x"))) if args.topology else None
-    ring = ProcessRing(layout, mask, topo, head_dim=d, transport=args.transport if world > 1 else None, slots=args.slots)
+    ring = ProcessRing(layout, mask, topo, head_dim=d, transport=args.transport if world > 1 else None, slots=args.slots,
+                       fanout=args.ce_fanout)
     n = layout.shard_size
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
 
@@ -366,6 +368,7 @@ def run_gpu(args) -> None:
         exposed = max(0.0, step_s - comp_s)
         overlap = {
             "transport": ring.transport,
+            "ce_fanout": ring.fanout if ring.transport == "ce" else None,
             "step_ms": step_s * 1e3, "compute_ms": comp_s * 1e3, "comm_alone_ms": comm_s * 1e3,
             "exposed_comm_ms": exposed * 1e3,
             "hidden_frac": (1.0 - min(exposed, comm_s) / comm_s) if comm_s > 0 else None,

@@ -126,17 +126,29 @@ class Channel:
         """Start a pass (every rank, same order): bumps the epoch the flags carry."""
         self.epoch += 1
 
-    def push(self, s: int, tensors: list[torch.Tensor], stream: torch.cuda.Stream) -> None:
-        """Copy-engine push of this rank's step-``s`` payload into ``send_to[s]``'s slot."""
+    def push(self, s: int, tensors: list[torch.Tensor], stream: torch.cuda.Stream, extra_streams=()) -> None:
+        """Copy-engine push of this rank's step-``s`` payload into ``send_to[s]``'s slot.
+        ``extra_streams`` split every tensor's bytes across more copy engines; the ready flag
+        is written on ``stream`` once all parts have landed."""
         lib, e, dst = self._lib, self.epoch, self.send_to[s]
         h = stream.cuda_stream
         if not (e == 1 and s <= self.slots):  # slot was used before: wait for the receiver's release
             _check(lib.bb_flag_wait(C.c_void_p(self._free(self.rank, s)), e, C.c_void_p(h)))
+        lanes = [stream] + list(extra_streams)
+        for x in lanes[1:]:
+            x.wait_stream(stream)  # payload produced + slot released
         base = self.peer_base[dst] + self._slot(s) * self.slot_bytes
         for t, (shape, dt), off, nb in zip(tensors, self.spec, self.offsets, self.sizes):
             if tuple(t.shape) != shape or t.dtype != dt or not t.is_contiguous():
                 raise ValueError(f"channel {self.name}: payload {tuple(t.shape)} {t.dtype} != {shape} {dt}")
-            _check(lib.bb_copy_async(C.c_void_p(base + off), C.c_void_p(t.data_ptr()), nb, C.c_void_p(h)))
+            part = _round_up(-(-nb // len(lanes)))
+            for i, x in enumerate(lanes):
+                lo, hi = i * part, min(nb, (i + 1) * part)
+                if hi > lo:
+                    _check(lib.bb_copy_async(C.c_void_p(base + off + lo), C.c_void_p(t.data_ptr() + lo), hi - lo,
+                                             C.c_void_p(x.cuda_stream)))
+        for x in lanes[1:]:
+            stream.wait_stream(x)
         _check(lib.bb_flag_write(C.c_void_p(self._ready(dst, s)), e, C.c_void_p(h)))
         self.bytes_pushed += self.payload_bytes
 

@@ -32,6 +32,7 @@ hop is one NVLink traversal, so both are the same bandwidth class.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -62,7 +63,8 @@ class ProcessRing:
     """Ring attention for one rank: ``forward`` -> (O, lse); ``backward`` -> (dQ, dK, dV)."""
 
     def __init__(self, layout: ShardLayout, mask: MaskSpec, topology: Topology | None = None, group=None,
-                 head_dim: int | None = None, transport: str | None = None, slots: int | None = None):
+                 head_dim: int | None = None, transport: str | None = None, slots: int | None = None,
+                 fanout: int | None = None):
         self.layout = layout
         self.mask = mask
         validate_mask(mask, layout.seq_len)
@@ -90,6 +92,7 @@ class ProcessRing:
             raise ValueError("the copy-engine transport needs CUDA devices")
         self.transport = transport
         self.slots = slots  # arena slots per channel (default world-1: every payload of a pass in flight)
+        self.fanout = max(1, int(fanout or os.environ.get("BB_CE_FANOUT", "1")))  # copy streams per push
         self._channels: dict = {}
         self._grad_state: dict = {}  # per gradient channel: partial buffers, their events, fold target
         self.split_own = True  # CE backward: own step split by kv heads around the remote steps
@@ -314,6 +317,7 @@ class ProcessRing:
         if self._xs_data is None:
             self._xs_data = torch.cuda.Stream(self.device)
             self._xs_grad = torch.cuda.Stream(self.device)
+            self._xs_lanes = [[torch.cuda.Stream(self.device) for _ in range(self.fanout - 1)] for _ in range(2)]
             self._xs_fold = torch.cuda.Stream(self.device, priority=-1)  # folds win the next free SM
         return torch.cuda.current_stream(self.device), self._xs_data, self._xs_grad
 
@@ -322,7 +326,7 @@ class ProcessRing:
         ch.begin()
         xs.wait_stream(cs)  # payload produced on the compute stream
         for s in range(1, self.world):
-            ch.push(s, list(payload), xs)
+            ch.push(s, list(payload), xs, self._xs_lanes[0])
         self.stats.bytes_sent += (self.world - 1) * ch.payload_bytes
 
     def _forward_ce(self, q, k, v, o, lse, d):
@@ -377,7 +381,7 @@ class ProcessRing:
                 self._launch(launch, payload, acc, j, None)
             dch.release(t, cs)
             xg.wait_stream(cs)
-            gch.push(t, list(acc), xg)
+            gch.push(t, list(acc), xg, self._xs_lanes[1])
             self.stats.bytes_sent += gch.payload_bytes
             if self.compute:
                 with torch.cuda.stream(xg):

@@ -230,7 +230,7 @@ def sim(monkeypatch):
     return SIM
 
 
-def make_rings(world, topo, slots, hq=2, hkv=2, n_per=8, d=4):
+def make_rings(world, topo, slots, hq=2, hkv=2, n_per=8, d=4, fanout=1):
     layout = ShardLayout("zigzag", n_per * world, world)
     rings = []
     for r in range(world):
@@ -245,7 +245,8 @@ def make_rings(world, topo, slots, hq=2, hkv=2, n_per=8, d=4):
         ring_mod.dist.get_world_size = lambda g=None: world
         ring_mod.dist.get_rank = lambda g=None, _r=r: _r
         try:
-            ring.__init__(layout, M.causal_mask(), Topology(*topo), head_dim=d, transport="collective", slots=slots)
+            ring.__init__(layout, M.causal_mask(), Topology(*topo), head_dim=d, transport="collective", slots=slots,
+                          fanout=fanout)
         finally:
             ring_mod.dist.is_initialized, ring_mod.dist.get_world_size, ring_mod.dist.get_rank = orig
         ring.transport = "ce"
@@ -272,9 +273,9 @@ def run_pass(rings, data, what):
 
 
 @pytest.mark.parametrize("world,topo", [(2, (1, 2)), (3, (1, 3)), (4, (1, 4)), (4, (2, 2)), (8, (1, 8)), (8, (2, 4)), (8, (4, 2))])
-@pytest.mark.parametrize("slots", [None, 1, 2])
-def test_ce_schedule_drains(sim, world, topo, slots):
-    rings, data = make_rings(world, topo, slots, hq=4, hkv=2)
+@pytest.mark.parametrize("slots,fanout", [(None, 1), (1, 1), (2, 1), (None, 3)])
+def test_ce_schedule_drains(sim, world, topo, slots, fanout):
+    rings, data = make_rings(world, topo, slots, hq=4, hkv=2, fanout=fanout)
     passes = ["forward", BURST_BACKWARD, "forward", RING_BACKWARD, "forward", BURST_BACKWARD, "forward", RING_BACKWARD]
     for i, what in enumerate(passes):
         run_pass(rings, data, what)
