@@ -6,8 +6,9 @@
 A step = one BurstAttention forward ring pass + one burst backward ring pass over
 the whole sequence (BASELINE.json configs[1]: LLaMA-7B attention, 32 heads,
 d=128, 128K tokens, causal, zigzag, bf16).  N=1 runs the whole sequence on one
-GPU; N>1 (torchrun, one rank per GPU, NCCL over NVLink) shards the same
-sequence over N ranks (strong scaling) through paper_2509_19836_b200.ring.
+GPU; N>1 (torchrun, one rank per GPU) shards the same sequence over N ranks
+(strong scaling) through paper_2509_19836_b200.ring; the ring exchange runs on
+the copy engines over NVLink (--transport ce, default) or NCCL (collective).
 
 value      whole-job algorithmic TFLOP/s = 14*d*H*P*K / max-over-ranks time
            (P = exact unmasked pairs; FlashAttention convention, SURVEY §8d);
@@ -33,6 +34,10 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# The ring's copy / fold streams block on flag words (cuStreamWaitValue32); give every stream
+# its own hardware queue so a parked wait never holds up an unrelated stream (read at CUDA
+# context creation, i.e. before torch touches the GPU).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 DENSE_BF16_PEAK = 2250.0  # TFLOP/s, B200 datasheet (MFU denominator)
 

@@ -7,6 +7,8 @@ Exits non-zero on mismatch.  Used by tests/test_ring_multigpu.py when >= 2 GPUs 
 import os
 import sys
 
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # see bench.py
+
 import numpy as np
 import torch
 import torch.distributed as dist
