@@ -1,0 +1,57 @@
+"""`python -m paper_2509_19836_b200 comm|balance` reproduces the reference CLI's reports byte for
+byte (json / csv / table, exit codes and error lines), against golden outputs of
+burstsim/cli.py made by tests/golden/make_cli_golden.py."""
+
+import contextlib
+import io
+import json
+from pathlib import Path
+
+import pytest
+
+from paper_2509_19836_b200.cli import main
+
+GOLDEN = json.loads((Path(__file__).parent / "golden" / "cli_golden.json").read_text())
+
+
+@pytest.mark.parametrize("name", sorted(GOLDEN))
+def test_cli_report_matches_reference(name):
+    case = GOLDEN[name]
+    so, se = io.StringIO(), io.StringIO()
+    with contextlib.redirect_stdout(so), contextlib.redirect_stderr(se):
+        rc = main(case["argv"])
+    assert rc == case["rc"]
+    assert so.getvalue() == case["stdout"]
+    assert se.getvalue() == case["stderr"]
+
+
+def test_timeline_needs_a_gpu_or_reports_one(tmp_path):
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("covered by the GPU suite")
+    se = io.StringIO()
+    with contextlib.redirect_stderr(se):
+        rc = main(["timeline", "--seq", "64", "--dim", "8", "--format", "json"])
+    assert rc == 2 and "needs a CUDA device" in se.getvalue()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pass_kind", ["forward", "burst_backward"])
+def test_timeline_is_measured_on_the_gpu(pass_kind):
+    """The timeline subcommand runs one ring pass on the GPU(s) and reports CUDA-event times in
+    the reference's schema; its traffic section equals the reference's element model."""
+    from paper_2509_19836_b200.fabric import account_attention_comm
+
+    so = io.StringIO()
+    with contextlib.redirect_stdout(so):
+        rc = main(["timeline", "--seq", "4096", "--dim", "128", "--gpus", "2", "--pass", pass_kind, "--format", "json"])
+    assert rc == 0
+    doc = json.loads(so.getvalue())
+    assert doc["schema_version"] == 1 and doc["params"]["makespan_seconds"] > 0
+    sec = {s["name"]: s for s in doc["sections"]}
+    kinds = {row[1] for row in sec["events"]["rows"]}
+    assert "compute" in kinds
+    assert all(row[3] >= row[2] >= 0 for row in sec["events"]["rows"])
+    sent = sum(r[1] + r[2] for r in sec["traffic"]["rows"])
+    assert sent == account_attention_comm(pass_kind, 4096, 128, 2)
