@@ -179,6 +179,14 @@ int bb_lmhead_fused(const bb_lmhead_args* args, void* stream);
 int bb_gemm_bf16(const void* a, const void* b, float* c, int64_t m, int64_t n, int64_t k,
                  int32_t a_mn, int32_t b_mn, int32_t accumulate, void* stream);
 
+/* Projection GEMM with the layout permutation and the bf16 cast fused into its store
+ * (replaces oracle.project_qkv's matmul + shard_rows' row gather, oracle.py:60-65,
+ * distributed.py:104-117): C[row_map[i], :] = bf16(A[i, :] . B^T) for i < m, with A
+ * bf16 [m, k] K-major and B bf16 [n, k] (b_mn == 0) or [k, n] (b_mn != 0); row_map
+ * (device int64 [m], may be NULL = identity) sends token row i to its shard-major row. */
+int bb_gemm_bf16_rows(const void* a, const void* b, void* c, const int64_t* row_map, int64_t m, int64_t n, int64_t k,
+                      int32_t b_mn, void* stream);
+
 /* ---- Peer fabric for the one-process-per-GPU ring (csrc/bb_fabric.cu) ----
  * Replaces the reference's payload "send" of a ring step (TransferStep /
  * MessageLog, fabric.py:180-226; distributed.py:176-177, 283-286) with a

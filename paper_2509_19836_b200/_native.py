@@ -29,6 +29,7 @@ EXPORTS = (
     "bb_lmhead_workspace_bytes",
     "bb_lmhead_fused",
     "bb_gemm_bf16",
+    "bb_gemm_bf16_rows",
     "bb_ipc_handle_bytes",
     "bb_arena_alloc",
     "bb_arena_free",
@@ -151,6 +152,7 @@ def load(path: os.PathLike | str | None = None) -> C.CDLL:
     lib.bb_lmhead_workspace_bytes.restype = i64
     lib.bb_lmhead_fused.argtypes = [C.POINTER(BbLmheadArgs), vp]
     lib.bb_gemm_bf16.argtypes = [vp, vp, vp, i64, i64, i64, i32, i32, i32, vp]
+    lib.bb_gemm_bf16_rows.argtypes = [vp, vp, vp, vp, i64, i64, i64, i32, vp]
     lib.bb_ipc_handle_bytes.restype = i32
     lib.bb_arena_alloc.argtypes = [i64, C.POINTER(vp)]
     lib.bb_arena_free.argtypes = [vp]

@@ -189,6 +189,11 @@ int bb_gemm_bf16(const void* a, const void* b, float* c, int64_t m, int64_t n, i
                      accumulate ? GEMM_ACCUM : GEMM_STORE, nullptr, false, static_cast<cudaStream_t>(stream));
 }
 
+int bb_gemm_bf16_rows(const void* a, const void* b, void* c, const int64_t* row_map, int64_t m, int64_t n, int64_t k,
+                      int32_t b_mn, void* stream) {
+  return launch_gemm_bf16(a, b, c, row_map, m, n, k, k, b_mn ? n : k, n, b_mn != 0, static_cast<cudaStream_t>(stream));
+}
+
 static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 struct LmWorkspace {

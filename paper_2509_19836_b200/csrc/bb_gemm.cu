@@ -33,6 +33,8 @@ constexpr int THREADS = 256;
 struct GemmArgs {
   int64_t m, n, k, ldc;
   float* c;
+  __nv_bfloat16* c16;       // GEMM_BF16: bf16 output, row grow written to row row_map[grow]
+  const int64_t* row_map;   // (identity when null)
   LogitsEpilogue le;
   int tiles_m, tiles_n;
   bool raster_m_fast;
@@ -175,6 +177,20 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         const int64_t col0 = n0 + c * 32;
         if (!row_ok || col0 >= p.n) continue;
+        if (EPI == GEMM_BF16) {  // cast + row permutation fused into the store
+          __nv_bfloat16* d16 = p.c16 + (p.row_map ? p.row_map[grow] : grow) * p.ldc + col0;
+          if (col0 + 32 <= p.n && (p.ldc % 8) == 0) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              reinterpret_cast<uint4*>(d16)[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          } else {
+            for (int i = 0; i < 32 && col0 + i < p.n; ++i) d16[i] = __float2bfloat16_rn(v[i]);
+          }
+          continue;
+        }
         float* dst = p.c ? p.c + grow * p.ldc + col0 : nullptr;
         const bool full_chunk = col0 + 32 <= p.n;
         if (EPI == GEMM_LOGITS) {
@@ -386,6 +402,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         const int64_t col0 = n0 + c * 32;
         if (!row_ok || col0 >= p.n) continue;
+        if (EPI == GEMM_BF16) {  // cast + row permutation fused into the store
+          __nv_bfloat16* d16 = p.c16 + (p.row_map ? p.row_map[grow] : grow) * p.ldc + col0;
+          if (col0 + 32 <= p.n && (p.ldc % 8) == 0) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              reinterpret_cast<uint4*>(d16)[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          } else {
+            for (int i = 0; i < 32 && col0 + i < p.n; ++i) d16[i] = __float2bfloat16_rn(v[i]);
+          }
+          continue;
+        }
         float* dst = p.c ? p.c + grow * p.ldc + col0 : nullptr;
         const bool full_chunk = col0 + 32 <= p.n;
         if (EPI == GEMM_LOGITS) {
@@ -483,6 +513,32 @@ int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& ar
 }  // namespace
 
 int gemm_n_tile() { return BN; }
+
+int launch_gemm_bf16(const void* a, const void* b, void* c16, const int64_t* row_map, int64_t m, int64_t n, int64_t k,
+                     int64_t lda, int64_t ldb, int64_t ldc, bool b_mn, cudaStream_t stream) {
+  if (m <= 0 || n <= 0 || k <= 0) return set_error(BB_ERR_INVALID, "gemm: empty problem %lld x %lld x %lld", (long long)m, (long long)n, (long long)k);
+  if ((lda * 2) % 16 || (ldb * 2) % 16)
+    return set_error(BB_ERR_INVALID, "gemm: leading dimensions must be multiples of 8 elements");
+  CUtensorMap ta, tb;
+  const bool pair = BB_GEMM_PAIR && m >= 2 * BM;
+  bool ok = make_tmap_bf16_2d(&ta, a, k, m, lda * 2, 64, BM);
+  ok = ok && (b_mn ? make_tmap_bf16_2d(&tb, b, n, k, ldb * 2, 64, 64)
+                   : make_tmap_bf16_2d(&tb, b, k, n, ldb * 2, 64, pair ? 128 : BN));
+  if (!ok) return BB_ERR_CUDA;
+  GemmArgs args{};
+  args.m = m;
+  args.n = n;
+  args.k = k;
+  args.ldc = ldc;
+  args.c16 = static_cast<__nv_bfloat16*>(c16);
+  args.row_map = row_map;
+  args.tiles_m = static_cast<int>((m + BM - 1) / BM);
+  args.tiles_n = static_cast<int>((n + BN - 1) / BN);
+  args.raster_m_fast = false;
+  args.pair = pair;
+  return b_mn ? launch_impl<false, true, GEMM_BF16>(ta, tb, args, stream)
+              : launch_impl<false, false, GEMM_BF16>(ta, tb, args, stream);
+}
 
 int launch_gemm(const void* a, const void* b, float* c, int64_t m, int64_t n, int64_t k, int64_t lda,
                 int64_t ldb, int64_t ldc, bool a_mn, bool b_mn, int epilogue, const LogitsEpilogue* le,

@@ -33,7 +33,7 @@ int num_sms();
 long long* debug_probe_buffer();
 
 // ---- launchers (one per kernel family) ----
-enum GemmEpilogue { GEMM_STORE = 0, GEMM_ACCUM = 1, GEMM_LOGITS = 2 };
+enum GemmEpilogue { GEMM_STORE = 0, GEMM_ACCUM = 1, GEMM_LOGITS = 2, GEMM_BF16 = 3 };
 
 struct LogitsEpilogue {
   const int64_t* targets;  // [M] vocab ids for the rows of this tile
@@ -46,6 +46,9 @@ int launch_gemm(const void* a, const void* b, float* c, int64_t m, int64_t n, in
                 int64_t lda, int64_t ldb, int64_t ldc, bool a_mn, bool b_mn, int epilogue,
                 const LogitsEpilogue* le, bool raster_m_fast, cudaStream_t stream);
 int gemm_n_tile();
+// C16[row_map ? row_map[i] : i, :] = bf16(A[i, :] . B^T); A K-major, B K-major or MN-major.
+int launch_gemm_bf16(const void* a, const void* b, void* c16, const int64_t* row_map, int64_t m, int64_t n, int64_t k,
+                     int64_t lda, int64_t ldb, int64_t ldc, bool b_mn, cudaStream_t stream);
 
 int launch_attn_fwd(const bb_attn_fwd_args& a, cudaStream_t stream);
 int launch_attn_bwd(const bb_attn_bwd_args& a, cudaStream_t stream);

@@ -1,0 +1,219 @@
+"""The callers either side of the ring: burstsim.oracle's layer entry points on
+the B200 kernels, and the QKV projection with the layout permutation fused into its GEMM.
+
+* ``AttentionParams`` / ``project_qkv`` (oracle.py:29-44, 60-65): (Q, K, V) = (X Wq, X Wk, X Wv)
+  on the tcgen05 GEMM (bf16 operands, fp32 accumulation).
+* ``project_qkv_shards``: the same projection for a sharded sequence, where the GEMM's
+  store writes token row r straight to its shard-major row (``bb_gemm_bf16_rows`` with the
+  inverse of ``shard_token_arrays``' gather) and casts to bf16 — the shards come out of the
+  projection in the layout the ring kernels read, with no separate permutation pass over HBM
+  (``shard_rows``, distributed.py:104-117, is a gather of the projected matrix).
+* ``attention_forward`` / ``attention_backward`` (oracle.py:80-119): exact single-device masked
+  attention through the ring-step kernels with one device (G = 1).
+
+NumPy inputs give float64 NumPy outputs like the reference; values carry bf16 input rounding
+(DESIGN.md §3 tolerances).  CUDA tensors are used in place.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import kernels as K
+from .distributed import AttentionGrads, AttentionResult
+from .masks import BLOCK_SPARSE, MaskSpec, validate_mask
+from .partitioning import ShardLayout, device_token_ids
+
+
+@dataclass(frozen=True)
+class AttentionParams:
+    """Square input/output projections of one attention layer (oracle.py:29-44)."""
+
+    dim: int
+    w_q: np.ndarray
+    w_k: np.ndarray
+    w_v: np.ndarray
+    w_attn: np.ndarray
+
+    def __post_init__(self):
+        for name in ("w_q", "w_k", "w_v", "w_attn"):
+            w = getattr(self, name)
+            if tuple(w.shape) != (self.dim, self.dim):
+                raise ValueError(f"{name} must be {self.dim}x{self.dim}, got {tuple(w.shape)}")
+
+
+def _device(device) -> torch.device:
+    if device is not None:
+        return torch.device(device)
+    if not torch.cuda.is_available():
+        raise RuntimeError("burst-b200 needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _matrix(x, name: str) -> np.ndarray | torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        if x.dim() != 2:
+            raise ValueError(f"{name} must be a 2-D matrix, got shape {tuple(x.shape)}")
+        return x
+    a = np.asarray(x, dtype=np.float64)
+    if a.ndim != 2:
+        raise ValueError(f"{name} must be a 2-D matrix, got shape {a.shape}")
+    return a
+
+
+def _bf16_padded(x, dev: torch.device, cols: int) -> torch.Tensor:
+    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+    t = t.to(device=dev, dtype=torch.float32)
+    if t.shape[1] < cols:
+        t = torch.nn.functional.pad(t, (0, cols - t.shape[1]))
+    return t.to(torch.bfloat16).contiguous()
+
+
+def gemm_rows(x: torch.Tensor, w: torch.Tensor, out: torch.Tensor, row_map: torch.Tensor | None = None) -> None:
+    """out[row_map[i]] = bf16(x[i] . w) on the tcgen05 GEMM: x bf16 [m, k], w bf16 [k, n]
+    (stored as given, i.e. MN-major B), out bf16 [rows, n]; see bb_gemm_bf16_rows."""
+    for t, name in ((x, "x"), (w, "w"), (out, "out")):
+        if not t.is_cuda or t.dtype != torch.bfloat16 or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous bf16 CUDA tensor")
+    m, k = x.shape
+    n = w.shape[1]
+    if w.shape[0] != k or out.shape[1] != n:
+        raise ValueError(f"gemm_rows: shapes x {tuple(x.shape)}, w {tuple(w.shape)}, out {tuple(out.shape)} disagree")
+    if row_map is not None and (row_map.dtype != torch.int64 or not row_map.is_cuda or row_map.shape != (m,)):
+        raise ValueError("row_map must be a CUDA int64 vector with one entry per row of x")
+    stream = torch.cuda.current_stream(x.device).cuda_stream
+    N.check(N.load().bb_gemm_bf16_rows(x.data_ptr(), w.data_ptr(), out.data_ptr(),
+                                       None if row_map is None else row_map.data_ptr(), m, n, k, 1, C.c_void_p(stream)))
+
+
+def _weights(params: AttentionParams, dev: torch.device, kp: int, np_: int) -> list[torch.Tensor]:
+    out = []
+    for w in (params.w_q, params.w_k, params.w_v):
+        t = w if isinstance(w, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(w, dtype=np.float64))
+        t = torch.nn.functional.pad(t.to(device=dev, dtype=torch.float32), (0, np_ - t.shape[1], 0, kp - t.shape[0]))
+        out.append(t.to(torch.bfloat16).contiguous())
+    return out
+
+
+def project_qkv(x, params: AttentionParams, device=None):
+    """(Q, K, V) = (X Wq, X Wk, X Wv) (oracle.py:60-65) on the GPU GEMM."""
+    x = _matrix(x, "input embeddings")
+    if x.shape[1] != params.dim:
+        raise ValueError(f"input has {x.shape[1]} columns, params expect {params.dim}")
+    dev = _device(device)
+    d = params.dim
+    kp = np_ = -(-d // 8) * 8  # TMA rows are 16-byte multiples
+    xb = _bf16_padded(x, dev, kp)
+    outs = []
+    for w in _weights(params, dev, kp, np_):
+        o = torch.empty(x.shape[0], np_, dtype=torch.bfloat16, device=dev)
+        gemm_rows(xb, w, o)
+        outs.append(o[:, :d])
+    if isinstance(x, torch.Tensor):
+        return tuple(outs)
+    return tuple(o.double().cpu().numpy() for o in outs)
+
+
+def project_qkv_shards(x, params: AttentionParams, layout: ShardLayout, heads: int = 1, device=None):
+    """Projection of the whole sequence straight into per-device shards: returns G tuples
+    (Q_i, K_i, V_i) of bf16 [n, heads, dim/heads] CUDA tensors holding the rows of device i in
+    shard order (``shard_token_arrays``), written by the GEMM's permuting bf16 store."""
+    x = _matrix(x, "input embeddings")
+    if x.shape[1] != params.dim:
+        raise ValueError(f"input has {x.shape[1]} columns, params expect {params.dim}")
+    if x.shape[0] != layout.seq_len:
+        raise ValueError(f"input has {x.shape[0]} rows, layout expects {layout.seq_len}")
+    if params.dim % heads or (params.dim // heads) % 8:
+        raise ValueError(f"dim {params.dim} must split into {heads} heads of a multiple of 8")
+    dev = _device(device)
+    d, g, n = params.dim, layout.devices, layout.shard_size
+    gather = np.concatenate([device_token_ids(layout, i + 1) - 1 for i in range(g)])
+    row_map = np.empty_like(gather)
+    row_map[gather] = np.arange(gather.size)  # token row -> shard-major row
+    rmap = torch.from_numpy(row_map.astype(np.int64)).to(dev)
+    xb = _bf16_padded(x, dev, d)
+    bufs = []
+    for w in _weights(params, dev, d, d):
+        o = torch.empty(layout.seq_len, d, dtype=torch.bfloat16, device=dev)
+        gemm_rows(xb, w, o, rmap)
+        bufs.append(o)
+    return [tuple(b[i * n:(i + 1) * n].view(n, heads, d // heads) for b in bufs) for i in range(g)]
+
+
+def _first_empty_row(mask: MaskSpec, nq: int, nk: int) -> int | None:
+    """0-based first query row with no allowed key (only block-sparse masks can have one)."""
+    if mask.kind != BLOCK_SPARSE:
+        return None
+    bm = np.asarray(mask.block_mask) != 0
+    bl = int(mask.block_len)
+    for r in range(nq):
+        blk = bm[r // bl, : -(-nk // bl)]
+        if not blk.any():
+            return r
+    return None
+
+
+def attention_forward(q, k, v, mask: MaskSpec, device=None) -> AttentionResult:
+    """O = softmax(Q K^T / sqrt(d)) V and the row LSE (oracle.py:80-95), one device."""
+    q, k, v = _matrix(q, "Q"), _matrix(k, "K"), _matrix(v, "V")
+    if k.shape[0] != v.shape[0]:
+        raise ValueError(f"K has {k.shape[0]} rows but V has {v.shape[0]}")
+    if q.shape[1] != k.shape[1] or k.shape[1] != v.shape[1]:
+        raise ValueError("Q, K, V must share the model dimension")
+    nq, nk, d = q.shape[0], k.shape[0], q.shape[1]
+    validate_mask(mask, max(nq, nk))
+    if nq > nk:
+        raise ValueError(f"{nq} query rows > {nk} keys: the ring kernels take at most one query per key row")
+    bad = _first_empty_row(mask, nq, nk)
+    if bad is not None:
+        raise ValueError(f"query row {bad + 1} has no unmasked key")
+    dev = _device(device)
+    dp = 64 if d <= 64 else 128
+    if d > 128:
+        raise ValueError(f"model dimension {d} > 128: split it into heads (the kernels take d <= 128)")
+    qb, kb, vb = (_bf16_padded(t, dev, dp).view(-1, 1, dp) for t in (q, k, v))
+    layout = ShardLayout("contiguous", nk, 1)
+    o = torch.zeros(nq, 1, dp, device=dev)
+    lse = torch.full((1, nq), float("-inf"), device=dev)
+    K.attn_fwd_step(qb, kb, vb, o, lse, layout, K.device_mask(mask, dev), 1, 1, 1.0 / math.sqrt(d), n_q=nq)
+    res = AttentionResult(o=o[:, 0, :d], lse=lse[0])
+    if isinstance(q, torch.Tensor):
+        return res
+    return AttentionResult(o=res.o.double().cpu().numpy(), lse=res.lse.double().cpu().numpy())
+
+
+def attention_backward(q, k, v, o, lse, do, mask: MaskSpec, device=None) -> AttentionGrads:
+    """Gradients of sum(O * dO) w.r.t. Q, K, V (oracle.py:98-119), one device."""
+    q, k, v, do = _matrix(q, "Q"), _matrix(k, "K"), _matrix(v, "V"), _matrix(do, "dO")
+    o = _matrix(o, "O")
+    if tuple(do.shape) != (q.shape[0], v.shape[1]):
+        raise ValueError(f"dO must be {q.shape[0]}x{v.shape[1]}, got {tuple(do.shape)}")
+    nq, nk, d = q.shape[0], k.shape[0], q.shape[1]
+    if nq > nk:
+        raise ValueError(f"{nq} query rows > {nk} keys: the ring kernels take at most one query per key row")
+    if d > 128:
+        raise ValueError(f"model dimension {d} > 128: split it into heads (the kernels take d <= 128)")
+    dev = _device(device)
+    dp = 64 if d <= 64 else 128
+    qb, kb, vb, dob = (_bf16_padded(t, dev, dp).view(-1, 1, dp) for t in (q, k, v, do))
+    ot = o if isinstance(o, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(o))
+    ot = torch.nn.functional.pad(ot.to(device=dev, dtype=torch.float32), (0, dp - d)).view(-1, 1, dp).contiguous()
+    lt = lse if isinstance(lse, torch.Tensor) else torch.from_numpy(np.asarray(lse, dtype=np.float64))
+    lt = lt.to(device=dev, dtype=torch.float32).reshape(1, nq).contiguous()
+    layout = ShardLayout("contiguous", nk, 1)
+    delta = torch.empty(1, nq, device=dev)
+    K.bwd_preprocess(dob, ot, delta)
+    dq = torch.zeros(nq, 1, dp, device=dev)
+    dk = torch.zeros(nk, 1, dp, device=dev)
+    dv = torch.zeros(nk, 1, dp, device=dev)
+    K.attn_bwd_step(qb, kb, vb, dob, lt, delta, dq, dk, dv, layout, K.device_mask(mask, dev), 1, 1, 1.0 / math.sqrt(d))
+    grads = AttentionGrads(dq=dq[:, 0, :d], dk=dk[:, 0, :d], dv=dv[:, 0, :d])
+    if isinstance(q, torch.Tensor):
+        return grads
+    return AttentionGrads(*(t.double().cpu().numpy() for t in (grads.dq, grads.dk, grads.dv)))

@@ -1,0 +1,87 @@
+"""burstsim.oracle's layer entry points on the GPU (paper_2509_19836_b200.layer) against the CPU
+oracle: project_qkv, the permutation-fused project_qkv_shards (bit-exact against projecting
+then gathering), attention_forward / attention_backward (bf16 tolerances)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import burst_oracle as O
+from paper_2509_19836_b200 import layer as Lyr
+from paper_2509_19836_b200.masks import block_sparse_mask, causal_mask, full_mask, sliding_window_mask
+from paper_2509_19836_b200.partitioning import ShardLayout, device_token_ids
+
+pytestmark = pytest.mark.gpu
+
+
+def _bf16(a):
+    return torch.from_numpy(a).float().to(torch.bfloat16).double().numpy()
+
+
+def _params(d, seed=0):
+    rng = np.random.default_rng(seed)
+    w = [_bf16(rng.uniform(-1, 1, (d, d)) / np.sqrt(d)) for _ in range(4)]
+    return Lyr.AttentionParams(d, *w)
+
+
+@pytest.mark.parametrize("n,d", [(256, 64), (1000, 128), (77, 40)])
+def test_project_qkv_matches_matmul(n, d):
+    p = _params(d)
+    x = _bf16(np.random.default_rng(1).uniform(-1, 1, (n, d)))
+    q, k, v = Lyr.project_qkv(x, p)
+    for got, w in zip((q, k, v), (p.w_q, p.w_k, p.w_v)):
+        want = x @ w
+        assert got.shape == want.shape
+        assert np.abs(got - want).max() <= 1e-2 * max(1.0, np.abs(want).max())
+
+
+@pytest.mark.parametrize("kind,g,block", [("zigzag", 4, None), ("striped", 2, None), ("block_striped", 4, 64)])
+def test_project_qkv_shards_is_the_permuted_projection(kind, g, block):
+    n, d, heads = 2048, 128, 2
+    p = _params(d, 3)
+    x = _bf16(np.random.default_rng(2).uniform(-1, 1, (n, d)))
+    layout = ShardLayout(kind, n, g, block)
+    shards = Lyr.project_qkv_shards(x, p, layout, heads=heads)
+    full = Lyr.project_qkv(torch.from_numpy(x).cuda(), p)  # identity row map, same GEMM tiles
+    for i, (qi, ki, vi) in enumerate(shards):
+        rows = torch.from_numpy(device_token_ids(layout, i + 1) - 1).cuda()
+        for got, f in zip((qi, ki, vi), full):
+            assert got.shape == (n // g, heads, d // heads) and got.is_contiguous()
+            assert torch.equal(got.reshape(n // g, d), f.index_select(0, rows))  # bit-exact
+
+
+@pytest.mark.parametrize("mname", ["causal", "full", "window", "block"])
+@pytest.mark.parametrize("nq,nk,d", [(512, 512, 128), (300, 300, 64), (200, 384, 96)])
+def test_attention_forward_backward_match_oracle(mname, nq, nk, d):
+    rng = np.random.default_rng(5)
+    q, do = (_bf16(rng.uniform(-1, 1, (nq, d))) for _ in range(2))
+    k, v = (_bf16(rng.uniform(-1, 1, (nk, d))) for _ in range(2))
+    n = max(nq, nk)
+    if mname == "block":
+        bl = 64 if n % 64 == 0 else 60
+        nb = -(-n // bl)
+        bm = np.tril(np.ones((nb, nb), dtype=np.int64))
+        mask = block_sparse_mask(bm, bl)
+        dense = np.kron(bm, np.ones((bl, bl)))[:nq, :nk] != 0
+    else:
+        mask = {"causal": causal_mask(), "full": full_mask(), "window": sliding_window_mask(50)}[mname]
+        mt = {"causal": ("causal", None, None, None), "full": ("full", None, None, None),
+              "window": ("sliding_window", 50, None, None)}[mname]
+        dense = O.allowed(mt, np.arange(1, nq + 1), np.arange(1, nk + 1))
+    o_ref, lse_ref = O.attention_forward(q, k, v, dense)
+    res = Lyr.attention_forward(q, k, v, mask)
+    assert np.abs(res.o - o_ref).max() < 1e-2
+    assert np.abs(res.lse - lse_ref).max() < 2e-3
+    dq_ref, dk_ref, dv_ref = O.attention_backward(q, k, v, o_ref, lse_ref, do, dense)
+    gr = Lyr.attention_backward(q, k, v, res.o, res.lse, do, mask)
+    for got, want in ((gr.dq, dq_ref), (gr.dk, dk_ref), (gr.dv, dv_ref)):
+        assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-2
+
+
+def test_attention_forward_errors():
+    q = np.zeros((8, 16))
+    with pytest.raises(ValueError, match="K has 8 rows but V has 4"):
+        Lyr.attention_forward(q, q, np.zeros((4, 16)), causal_mask())
+    bm = np.array([[0, 0], [1, 1]])
+    with pytest.raises(ValueError, match="query row 1 has no unmasked key"):
+        Lyr.attention_forward(q, q, q, block_sparse_mask(bm, 4))
