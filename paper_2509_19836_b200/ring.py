@@ -434,6 +434,13 @@ class ProcessRing:
 
         self._grad_pass("kv", (k, v), "dkv", (dk, dv), launch, lambda j: not self.counts[self.rank, j], k.shape[1])
 
+    def close(self) -> None:
+        """Release the copy-engine arenas and peer mappings (collective-free; call after a sync)."""
+        for ch in self._channels.values():
+            ch.close()
+        self._channels.clear()
+        self._grad_state.clear()
+
     def _who_had_me(self, t: int) -> int:
         """Rank that computed on MY shard at step t (it sends me that gradient partial)."""
         return next(r for r in range(self.world) if ring_schedule(self.topology, r)[t] == self.rank)
