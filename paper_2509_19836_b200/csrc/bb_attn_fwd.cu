@@ -58,19 +58,31 @@ constexpr float RESCALE_THRESHOLD = 8.0f;
 // registers: s[128] per thread spilled ~230 B to local memory at the 168-register budget.
 #define BB_FWD_CHUNKED 0  // measured 10 % slower (1162 -> 1050 TF/s full 32K): the second TMEM pass costs more than the spills
 #endif
+#ifndef BB_FWD_SPLIT
+// Two softmax threads per query row (640 threads: 4 softmax warps per SMSP), each owning 64
+// of the 128 key columns: P of keys [64h, 64h+64) lands in S columns [64h, 64h+32), the row
+// max is exchanged through shared memory once per tile, S is re-read for the exp pass.
+#define BB_FWD_SPLIT 0  // measured 5 % slower (1110 vs 1165 TF/s full 32K, 995 vs 1039 causal 128K); parity-tested
+#endif
 #ifndef BB_FWD_PINGPONG
 #define BB_FWD_PINGPONG 0  // softmax warpgroups take turns on MUFU (named barriers 1, 2): measured 16 % slower (1159 -> 972 TF/s full 32K)
 #endif
 constexpr int POLY_EVERY = BB_POLY_EVERY;  // every POLY_EVERY-th P column uses ex2_poly (>8: never)  // log2 units: P may reach 2^8 before O is rescaled
 
-template <int D>
+template <bool SPLIT>
+constexpr int fwd_threads() { return SPLIT ? 640 : FWD_THREADS; }
+template <bool SPLIT>
+constexpr int kv_slots() { return SPLIT ? 4 : KV_SLOTS; }
+
+template <int D, bool SPLIT = false>
 struct FwdSmem {
   static constexpr uint32_t TILE = 128 * D * 2;  // one Q / K / V tile, D/64 panels of 16 KB
   static constexpr uint32_t Q_OFF = 0;
   static constexpr uint32_t KV_OFF = Q_OFF + 2 * TILE;
-  static constexpr uint32_t BAR_OFF = KV_OFF + KV_SLOTS * TILE;
+  static constexpr uint32_t BAR_OFF = KV_OFF + kv_slots<SPLIT>() * TILE;
   static constexpr uint32_t CLS_OFF = BAR_OFF + 256;  // per key tile: class(q tile 0) | class(q tile 1) << 2
-  static constexpr uint32_t BYTES = CLS_OFF + MAX_KT / 2;  // 4 bits per key tile
+  static constexpr uint32_t XCH_OFF = CLS_OFF + MAX_KT / 2;  // SPLIT: [parity][q tile][half][row] floats
+  static constexpr uint32_t BYTES = XCH_OFF + (SPLIT ? 2 * 2 * 2 * 128 * 4 : 0);
 };
 
 struct FwdParams {
@@ -99,12 +111,175 @@ __device__ __forceinline__ int32_t fwd_class(const FwdParams& p, int q, int64_t 
   return classify_tile(p.layout, p.mask, p.q_device, r0, r1, p.k_device, c0, c1, c1 - c0 == 128);
 }
 
-template <int D>
-__global__ void __launch_bounds__(FWD_THREADS, 1)
+// Softmax / correction / epilogue with two threads per query row (SPLIT): thread (q, h, row)
+// owns key columns [64h, 64h+64) of S and output columns [h*D/2, (h+1)*D/2) of O.
+template <int D, typename ClsFn>
+__device__ __forceinline__ void fwd_softmax_split(const FwdParams& p, uint8_t* xch_smem, uint32_t tmem, uint64_t* s_full,
+                                                  uint64_t* p_full, uint64_t* pv_done, int64_t m0, int64_t j_lo,
+                                                  int64_t j_hi, int head, ClsFn tile_cls) {
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int sw = static_cast<int>(warp) - 4;
+  const int q = sw >> 3, half = (sw >> 2) & 1;
+  const uint32_t quad = warp & 3;
+  const int row = quad * 32 + lane;
+  const int64_t qrow = m0 + 128 * q + row;
+  const bool row_ok = qrow < p.n_q;
+  const int64_t q_id = row_ok ? token_id(p.layout, p.q_device, qrow) : 0;
+  const uint32_t t_lane = (quad * 32) << 16;
+  const uint32_t s_col = tmem + t_lane + q * 128u + 64u * half;   // my 64 S columns
+  const uint32_t o_col = tmem + t_lane + 256u + q * D + (D / 2) * half;  // my D/2 O columns
+  float* xch = reinterpret_cast<float*>(xch_smem);  // [parity][q][half][row]
+  auto xslot = [&](uint32_t par, int hh) -> float& { return xch[((par * 2 + q) * 2 + hh) * 128 + row]; };
+  const float sl2 = p.scale_log2;
+  const uint32_t bar_id = 1 + q;  // the 256 threads of this query tile
+
+  float m_run = -INFINITY, l_run = 0.f;
+  uint32_t t = 0;
+  for (int64_t j = j_lo; j < j_hi; ++j) {
+    const int32_t cls = tile_cls(q, j);
+    if (cls == TILE_SKIP) continue;
+    mbar_wait(&s_full[q], t & 1);
+    tc_fence_after();
+    uint4 bits = make_uint4(~0u, ~0u, ~0u, ~0u);
+    if (cls == TILE_PARTIAL) bits = row_mask_bits(p.layout, p.mask, q_id, row_ok, p.k_device, j * 128, p.n_k, true);
+    float ca[32], cb[32];
+    auto mask32 = [&](float(&x)[32], int c0) {
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (!mask_bit(bits, c0 + c)) x[c] = -INFINITY;
+    };
+    tmem_ld32(s_col, ca);
+    tmem_ld32(s_col + 32, cb);
+    tmem_ld_wait();
+    reg_fence(ca);
+    reg_fence(cb);
+    if (cls == TILE_PARTIAL) {
+      mask32(ca, 64 * half);
+      mask32(cb, 64 * half + 32);
+    }
+    float mx8[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) mx8[i] = fmax3(fmax3(ca[i], ca[i + 8], ca[i + 16]), fmax3(ca[i + 24], cb[i], cb[i + 8]), fmaxf(cb[i + 16], cb[i + 24]));
+    const float m_half = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
+    xslot(t & 1, half) = m_half;
+    named_bar_sync(bar_id, 256);
+    const float mx = fmaxf(m_half, xslot(t & 1, half ^ 1));
+    const float m_tile = mx * sl2;
+    const bool need = m_tile > m_run + RESCALE_THRESHOLD;  // identical in both halves of the row
+    float alpha = 1.f;
+    if (need) {
+      alpha = (m_run == -INFINITY) ? 0.f : ex2_approx(m_run - m_tile);
+      m_run = m_tile;
+      l_run *= alpha;
+    }
+    const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
+    if (t > 0) {
+      mbar_wait(&pv_done[q], (t - 1) & 1);
+      tc_fence_after();
+      if (__any_sync(0xffffffff, need)) {
+#pragma unroll 1
+        for (int c = 0; c < D / 64; ++c) {
+          float o[32];
+          tmem_ld32(o_col + c * 32, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] *= alpha;
+          tmem_st32(o_col + c * 32, o);
+        }
+        tmem_st_wait();
+      }
+    }
+    // exp pass: P of keys [64h, 64h+64) -> columns [64h, 64h+32) of this S region, which only
+    // this thread reads
+    float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    const float2 sl2x2 = make_float2(sl2, sl2), negm2 = make_float2(neg_m, neg_m);
+    auto exp32 = [&](const float(&x)[32], uint32_t dst) {
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float2 y = __ffma2_rn(make_float2(x[2 * i], x[2 * i + 1]), sl2x2, negm2);
+        const float2 e = make_float2(ex2_approx(y.x), ex2_approx(y.y));
+        acc4[i & 3] = __fadd2_rn(acc4[i & 3], e);
+        pk[i] = pack_bf16(e.x, e.y);
+      }
+      tmem_st16(dst, pk);
+    };
+    // S is re-read rather than kept live across the exchange barrier (96-register budget)
+    tmem_ld32(s_col, ca);
+    tmem_ld32(s_col + 32, cb);
+    tmem_ld_wait();
+    reg_fence(ca);
+    reg_fence(cb);
+    if (cls == TILE_PARTIAL) {
+      mask32(ca, 64 * half);
+      mask32(cb, 64 * half + 32);
+    }
+    exp32(ca, s_col);
+    exp32(cb, s_col + 16);
+    l_run += ((acc4[0].x + acc4[0].y) + (acc4[1].x + acc4[1].y)) + ((acc4[2].x + acc4[2].y) + (acc4[3].x + acc4[3].y));
+    tmem_st_wait();
+    tc_fence_before();
+    mbar_arrive(&p_full[q]);
+    ++t;
+  }
+
+  if (t > 0) {
+    float* lse_ptr = p.lse + static_cast<int64_t>(head) * p.n_q + qrow;
+    const float lse_prev = row_ok ? *lse_ptr : -INFINITY;  // read by both halves before half 0 writes
+    xslot(t & 1, half) = l_run;
+    named_bar_sync(bar_id, 256);
+    const float l_tot = l_run + xslot(t & 1, half ^ 1);
+    mbar_wait(&pv_done[q], (t - 1) & 1);
+    tc_fence_after();
+    const float lse_step = (l_tot > 0.f) ? (m_run * 0.69314718055994531f + logf(l_tot)) : -INFINITY;
+    float w_step = 0.f, w_old = 0.f, lse_new = -INFINITY;
+    const bool write = row_ok && lse_step != -INFINITY;
+    if (write) {
+      if (lse_prev == -INFINITY) {
+        lse_new = lse_step;
+        w_step = 1.f / l_tot;
+      } else {
+        const float hi = fmaxf(lse_prev, lse_step), lo = fminf(lse_prev, lse_step);
+        lse_new = hi + log1pf(expf(lo - hi));
+        w_step = expf(lse_step - lse_new) / l_tot;
+        w_old = expf(lse_prev - lse_new);
+      }
+    }
+    named_bar_sync(bar_id, 256);  // both halves have read lse_prev
+    if (write && half == 0) *lse_ptr = lse_new;
+    float* o_row = p.o + (qrow * p.hq + head) * static_cast<int64_t>(D) + (D / 2) * half;
+#pragma unroll 1
+    for (int c = 0; c < D / 64; ++c) {
+      float o[32];
+      tmem_ld32(o_col + c * 32, o);
+      tmem_ld_wait();
+      if (write) {
+        float4* dst = reinterpret_cast<float4*>(o_row + c * 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float4 r = make_float4(o[4 * i] * w_step, o[4 * i + 1] * w_step, o[4 * i + 2] * w_step, o[4 * i + 3] * w_step);
+          if (w_old != 0.f) {
+            const float4 prev = dst[i];
+            r.x += w_old * prev.x;
+            r.y += w_old * prev.y;
+            r.z += w_old * prev.z;
+            r.w += w_old * prev.w;
+          }
+          dst[i] = r;
+        }
+      }
+    }
+  }
+}
+
+template <int D, bool SPLIT>
+__global__ void __launch_bounds__(fwd_threads<SPLIT>(), 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                     const __grid_constant__ CUtensorMap tv, const FwdParams p) {
-  using L = FwdSmem<D>;
+  using L = FwdSmem<D, SPLIT>;
   constexpr int PANELS = D / 64;
+  constexpr int KV_SLOTS = kv_slots<SPLIT>();
+  constexpr int FWD_THREADS = fwd_threads<SPLIT>();
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023) != 0) __trap();
 
@@ -136,7 +311,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     }
     for (int k = 0; k < 2; ++k) {
       mbar_init(&s_full[k], 1);
-      mbar_init(&p_full[k], 128);
+      mbar_init(&p_full[k], SPLIT ? 256 : 128);
       mbar_init(&pv_done[k], 1);
     }
     fence_barrier_init();
@@ -225,7 +400,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {  // A = P: 16 keys (8 packed columns) per k-step
           const uint64_t bd = sw128_desc(v_base + ks * 2048, 16384, 1024);
-          umma_ts(tmem + (256u + q * D), tmem + q * 128u + ks * 8u, bd, idesc_o, (issued[q] | ks) != 0);
+          // P of 16 keys = 8 packed columns; SPLIT keeps keys [64h, 64h+64) in columns [64h, 64h+32)
+          const uint32_t pcol = SPLIT ? (ks < 4 ? ks * 8u : 64u + (ks - 4) * 8u) : ks * 8u;
+          umma_ts(tmem + (256u + q * D), tmem + q * 128u + pcol, bd, idesc_o, (issued[q] | ks) != 0);
         }
         umma_commit(&pv_done[q]);
       }
@@ -281,6 +458,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       cls[0] = cls_n[0];
       cls[1] = cls_n[1];
     }
+  } else if (SPLIT && warp >= 4) {
+    fwd_softmax_split<D>(p, smem + L::XCH_OFF, tmem, s_full, p_full, pv_done, m0, j_lo, j_hi, head, tile_cls);
   } else if (warp >= 4) {
     // ------------------------------------------------ softmax / correction / epilogue
     const int q = (warp - 4) >> 2;  // query tile of this warpgroup
@@ -608,18 +787,20 @@ int launch_fwd_d(const bb_attn_fwd_args& a, cudaStream_t st) {
   p.mask = make_maskd(a.mask);
   p.q_pairs = static_cast<int32_t>((a.n_q + 255) / 256);
   p.probe = debug_probe_buffer();
-  auto kern = attn_fwd_kernel<D>;
+  constexpr bool SPLIT = BB_FWD_SPLIT != 0;
+  using L = FwdSmem<D, SPLIT>;
+  auto kern = attn_fwd_kernel<D, SPLIT>;
   static uint64_t attr_done = 0;  // per device: the attribute is per-context
   int dev = 0;
   cudaGetDevice(&dev);
   if (!((attr_done >> dev) & 1)) {
-    if (check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdSmem<D>::BYTES),
+    if (check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES),
                    "attn_fwd smem attribute"))
       return BB_ERR_CUDA;
     attr_done |= uint64_t(1) << dev;
   }
   dim3 grid(p.q_pairs, a.hq);
-  kern<<<grid, FWD_THREADS, FwdSmem<D>::BYTES, st>>>(tq, tk, tv, p);
+  kern<<<grid, fwd_threads<SPLIT>(), L::BYTES, st>>>(tq, tk, tv, p);
   return check_launch("attn_fwd_kernel");
 }
 
