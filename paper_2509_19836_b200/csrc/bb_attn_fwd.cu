@@ -458,9 +458,10 @@ __global__ void __launch_bounds__(fwd_threads<SPLIT>(), 1)
       cls[0] = cls_n[0];
       cls[1] = cls_n[1];
     }
-  } else if (SPLIT && warp >= 4) {
-    fwd_softmax_split<D>(p, smem + L::XCH_OFF, tmem, s_full, p_full, pv_done, m0, j_lo, j_hi, head, tile_cls);
   } else if (warp >= 4) {
+    if constexpr (SPLIT) {
+      fwd_softmax_split<D>(p, smem + L::XCH_OFF, tmem, s_full, p_full, pv_done, m0, j_lo, j_hi, head, tile_cls);
+    } else {
     // ------------------------------------------------ softmax / correction / epilogue
     const int q = (warp - 4) >> 2;  // query tile of this warpgroup
     const uint32_t quad = warp & 3;
@@ -756,6 +757,7 @@ __global__ void __launch_bounds__(fwd_threads<SPLIT>(), 1)
         }
       }
     }
+    }  // !SPLIT
   }
 
   tc_fence_before();
