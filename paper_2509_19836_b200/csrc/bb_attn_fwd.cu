@@ -64,6 +64,9 @@ constexpr float RESCALE_THRESHOLD = 8.0f;
 // max is exchanged through shared memory once per tile, S is re-read for the exp pass.
 #define BB_FWD_SPLIT 0  // measured 5 % slower (1110 vs 1165 TF/s full 32K, 995 vs 1039 causal 128K); parity-tested
 #endif
+#ifndef BB_SPLIT_POLY
+#define BB_SPLIT_POLY 0
+#endif
 #ifndef BB_FWD_PINGPONG
 #define BB_FWD_PINGPONG 0  // softmax warpgroups take turns on MUFU (named barriers 1, 2): measured 16 % slower (1159 -> 972 TF/s full 32K)
 #endif
@@ -138,7 +141,9 @@ __device__ __forceinline__ void fwd_softmax_split(const FwdParams& p, uint8_t* x
   for (int64_t j = j_lo; j < j_hi; ++j) {
     const int32_t cls = tile_cls(q, j);
     if (cls == TILE_SKIP) continue;
+    if (row == 0 && half == 0) FWD_PROBE(t, 16 + 8 * q);
     mbar_wait(&s_full[q], t & 1);
+    if (row == 0 && half == 0) FWD_PROBE(t, 17 + 8 * q);
     tc_fence_after();
     uint4 bits = make_uint4(~0u, ~0u, ~0u, ~0u);
     if (cls == TILE_PARTIAL) bits = row_mask_bits(p.layout, p.mask, q_id, row_ok, p.k_device, j * 128, p.n_k, true);
@@ -162,7 +167,9 @@ __device__ __forceinline__ void fwd_softmax_split(const FwdParams& p, uint8_t* x
     for (int i = 0; i < 8; ++i) mx8[i] = fmax3(fmax3(ca[i], ca[i + 8], ca[i + 16]), fmax3(ca[i + 24], cb[i], cb[i + 8]), fmaxf(cb[i + 16], cb[i + 24]));
     const float m_half = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
     xslot(t & 1, half) = m_half;
+    if (row == 0 && half == 0) FWD_PROBE(t, 23 + 8 * q);
     named_bar_sync(bar_id, 256);
+    if (row == 0 && half == 0) FWD_PROBE(t, 22 + 8 * q);
     const float mx = fmaxf(m_half, xslot(t & 1, half ^ 1));
     const float m_tile = mx * sl2;
     const bool need = m_tile > m_run + RESCALE_THRESHOLD;  // identical in both halves of the row
@@ -175,6 +182,7 @@ __device__ __forceinline__ void fwd_softmax_split(const FwdParams& p, uint8_t* x
     const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
     if (t > 0) {
       mbar_wait(&pv_done[q], (t - 1) & 1);
+      if (row == 0 && half == 0) FWD_PROBE(t, 18 + 8 * q);
       tc_fence_after();
       if (__any_sync(0xffffffff, need)) {
 #pragma unroll 1
@@ -193,12 +201,16 @@ __device__ __forceinline__ void fwd_softmax_split(const FwdParams& p, uint8_t* x
     // this thread reads
     float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
     const float2 sl2x2 = make_float2(sl2, sl2), negm2 = make_float2(neg_m, neg_m);
+    const bool poly_ok = cls != TILE_PARTIAL;  // masked -inf scores need MUFU's exact 0
     auto exp32 = [&](const float(&x)[32], uint32_t dst) {
       uint32_t pk[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const float2 y = __ffma2_rn(make_float2(x[2 * i], x[2 * i + 1]), sl2x2, negm2);
-        const float2 e = make_float2(ex2_approx(y.x), ex2_approx(y.y));
+        // BB_SPLIT_POLY: every 4th pair on the FMA pipe (MUFU alone needs as many cycles per
+        // key tile as the tile's MMAs)
+        const float2 e = (BB_SPLIT_POLY && (i & 3) == 3 && poly_ok) ? ex2_poly2(y)
+                                                                     : make_float2(ex2_approx(y.x), ex2_approx(y.y));
         acc4[i & 3] = __fadd2_rn(acc4[i & 3], e);
         pk[i] = pack_bf16(e.x, e.y);
       }
@@ -216,10 +228,12 @@ __device__ __forceinline__ void fwd_softmax_split(const FwdParams& p, uint8_t* x
     }
     exp32(ca, s_col);
     exp32(cb, s_col + 16);
+    if (row == 0 && half == 0) FWD_PROBE(t, 20 + 8 * q);
     l_run += ((acc4[0].x + acc4[0].y) + (acc4[1].x + acc4[1].y)) + ((acc4[2].x + acc4[2].y) + (acc4[3].x + acc4[3].y));
     tmem_st_wait();
     tc_fence_before();
     mbar_arrive(&p_full[q]);
+    if (row == 0 && half == 0) FWD_PROBE(t, 19 + 8 * q);
     ++t;
   }
 
