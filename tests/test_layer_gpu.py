@@ -85,3 +85,19 @@ def test_attention_forward_errors():
     bm = np.array([[0, 0], [1, 1]])
     with pytest.raises(ValueError, match="query row 1 has no unmasked key"):
         Lyr.attention_forward(q, q, q, block_sparse_mask(bm, 4))
+
+
+def test_project_qkv_reference_cases():
+    """The reference's TestProjectQkv (tests/test_oracle.py:56-95) at bf16 precision: identity
+    weights return the (bf16-rounded) input, zero input gives zeros."""
+    from oracle.burst_oracle import seeded_random_matrix
+
+    d = 3
+    eye = np.eye(d)
+    x = seeded_random_matrix(5, d, 1)
+    q, k, v = Lyr.project_qkv(x, Lyr.AttentionParams(dim=d, w_q=eye, w_k=eye, w_v=eye, w_attn=eye))
+    for t in (q, k, v):
+        assert np.array_equal(t, _bf16(x))
+    p = Lyr.AttentionParams(2, *(seeded_random_matrix(2, 2, s) for s in (2, 3, 4)), np.eye(2))
+    q, k, v = Lyr.project_qkv(np.zeros((4, 2)), p)
+    assert not q.any() and not k.any() and not v.any()
