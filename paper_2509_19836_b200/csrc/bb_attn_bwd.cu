@@ -40,7 +40,7 @@ namespace {
 #endif
 constexpr int NG = BB_BWD_NG;
 #ifndef BB_BWD_MC
-#define BB_BWD_MC 0  // 2-CTA multicast clusters: +1 % but hang intermittently at small shards (tools/bwd_heads_check.py)
+#define BB_BWD_MC 0  // 2-CTA Q/dO multicast clusters: correct since the empty-range fix, but a wash (976 vs 968 full 32K, 952 vs 955 causal 128K)
 #endif
 constexpr bool MC = BB_BWD_MC;
 #ifndef BB_BWD_DQ128
@@ -220,7 +220,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
 
   // Work items: (query head of the GQA group, query tile) in order, skipping masked tiles.
+  // (nr == 0 must end at once: the class table is empty, and a head step must re-check the
+  // range -- reading an unwritten table entry once sent two CTAs of a multicast cluster down
+  // different item lists, a hang)
   auto next_active = [&](int64_t w) {
+    if (nr == 0) return n_work;
     for (;;) {
       if ((w & 0xFFFF) >= nr) w = ((w >> 16) + 1) << 16;
       if (w >= n_work) return n_work;

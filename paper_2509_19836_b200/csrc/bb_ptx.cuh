@@ -2,6 +2,7 @@
 // mbarriers, TMA tile loads, tcgen05 MMA / TMEM traffic and the UMMA
 // shared-memory / instruction descriptors.  Inline PTX only; no CUTLASS.
 #pragma once
+#include <cstdio>
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -40,7 +41,32 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef BB_MBAR_WATCHDOG
+#define BB_MBAR_WATCHDOG 0  // debug builds: report (printf) and trap on an mbarrier wait that never ends
+#endif
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if BB_MBAR_WATCHDOG
+  long long spins = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if (++spins == (1ll << 24)) {
+      printf("mbar watchdog: block (%d,%d) cluster rank %u thread %d bar smem 0x%x parity %u\n", blockIdx.x, blockIdx.y,
+             0u, threadIdx.x, smem_u32(bar), parity);
+    }
+    if (spins > (1ll << 26)) __trap();
+  }
+  return;
+#endif
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "LAB_WAIT:\n\t"
