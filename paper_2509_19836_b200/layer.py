@@ -120,6 +120,15 @@ def project_qkv(x, params: AttentionParams, device=None):
     return tuple(o.double().cpu().numpy() for o in outs)
 
 
+def shard_row_map(layout: ShardLayout) -> np.ndarray:
+    """int64 [N]: global token row -> its row in the shard-major concatenation of
+    ``shard_token_arrays`` (the inverse of the gather ``shard_rows`` performs)."""
+    gather = np.concatenate([device_token_ids(layout, i + 1) - 1 for i in range(layout.devices)])
+    row_map = np.empty_like(gather)
+    row_map[gather] = np.arange(gather.size)
+    return row_map.astype(np.int64)
+
+
 def project_qkv_shards(x, params: AttentionParams, layout: ShardLayout, heads: int = 1, device=None):
     """Projection of the whole sequence straight into per-device shards: returns G tuples
     (Q_i, K_i, V_i) of bf16 [n, heads, dim/heads] CUDA tensors holding the rows of device i in
@@ -133,10 +142,7 @@ def project_qkv_shards(x, params: AttentionParams, layout: ShardLayout, heads: i
         raise ValueError(f"dim {params.dim} must split into {heads} heads of a multiple of 8")
     dev = _device(device)
     d, g, n = params.dim, layout.devices, layout.shard_size
-    gather = np.concatenate([device_token_ids(layout, i + 1) - 1 for i in range(g)])
-    row_map = np.empty_like(gather)
-    row_map[gather] = np.arange(gather.size)  # token row -> shard-major row
-    rmap = torch.from_numpy(row_map.astype(np.int64)).to(dev)
+    rmap = torch.from_numpy(shard_row_map(layout)).to(dev)
     xb = _bf16_padded(x, dev, d)
     bufs = []
     for w in _weights(params, dev, d, d):

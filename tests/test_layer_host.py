@@ -14,3 +14,18 @@ def test_non_square_params_rejected():
 def test_square_params_accepted():
     p = AttentionParams(dim=2, w_q=np.eye(2), w_k=np.eye(2), w_v=np.eye(2), w_attn=np.eye(2))
     assert p.dim == 2
+
+
+@pytest.mark.parametrize("kind,n,g,bl", [("zigzag", 64, 4, None), ("striped", 48, 3, None), ("block_striped", 64, 2, 8),
+                                         ("contiguous", 16, 2, None)])
+def test_shard_row_map_inverts_the_shard_gather(kind, n, g, bl):
+    """The row map the projection GEMM stores through sends token row r to the shard-major row
+    that shard_rows' gather reads it from (bit-exact against the golden-pinned layouts)."""
+    from paper_2509_19836_b200.layer import shard_row_map
+    from paper_2509_19836_b200.partitioning import ShardLayout, shard_token_arrays
+
+    layout = ShardLayout(kind, n, g, bl)
+    rmap = shard_row_map(layout)
+    shard_major = np.concatenate([np.asarray(ids) - 1 for ids in shard_token_arrays(layout)])
+    assert sorted(rmap.tolist()) == list(range(n))
+    assert np.array_equal(rmap[shard_major], np.arange(n))
