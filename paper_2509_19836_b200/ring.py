@@ -307,6 +307,7 @@ class ProcessRing:
             from .peer import Channel
 
             if ch is not None:
+                self._quiesce()
                 ch.close()
             src, dst = (self._dst, self._src) if grad else (self._src, self._dst)
             ch = Channel(name, spec, src, dst, self.rank, self.world, self.device, self.group, self.slots)
@@ -434,8 +435,17 @@ class ProcessRing:
 
         self._grad_pass("kv", (k, v), "dkv", (dk, dv), launch, lambda j: not self.counts[self.rank, j], k.shape[1])
 
+    def _quiesce(self) -> None:
+        """Every rank's earlier passes have finished (so no peer still writes a flag or payload
+        into an arena about to be freed): device sync, then a host barrier.  Collective."""
+        torch.cuda.synchronize(self.device)
+        if dist.is_initialized():
+            dist.barrier(group=self.group)
+
     def close(self) -> None:
-        """Release the copy-engine arenas and peer mappings (collective-free; call after a sync)."""
+        """Release the copy-engine arenas and peer mappings.  Collective (every rank calls it)."""
+        if self._channels:
+            self._quiesce()
         for ch in self._channels.values():
             ch.close()
         self._channels.clear()

@@ -67,6 +67,7 @@ def main():
                     o, lse = ring.forward(q, k, v)
                     dq, dk, dv = ring.backward(q, k, v, do, o, lse, kind=backward)
             torch.cuda.synchronize()
+            ring.close()  # collective: frees the copy-engine arenas after every rank's passes
             failures += _report(rank, f"{kind} {topo} {mname} {backward} {transport} slots={slots}", o, lse, dq, dk, dv,
                                 ref, r, ring.stats.bytes_sent)
     dist.barrier()
