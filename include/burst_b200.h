@@ -12,11 +12,15 @@
  *   bb_attn_bwd_preprocess  distributed.py:274-275  D = rowsum_hadamard(dO, O), numerics.py:86-92
  *   bb_permute_rows         distributed.py:104-130  shard_rows / gather_rows / make_device_states
  *   bb_lmhead_fused         lmhead.py:41-93         fused_lmhead_loss (loss, dH, dW)
+ *   bb_gemm_bf16_rows       oracle.py:60-65 +       project_qkv with shard_rows' permutation
+ *                           distributed.py:104-117  fused into the GEMM store
+ *   bb_ipc_* / bb_arena_* / fabric.py:180-226       a ring step's payload transfer (copy
+ *   bb_copy_async / bb_flag_*                       engines over NVLink + stream-ordered flags)
  *
  * Conventions: plain device pointers and sizes, no torch types.  Token ids and
  * devices are 1-based (burstsim README "Conventions").  All functions take a
- * cudaStream_t as `void*` (NULL = legacy default stream), never allocate, never
- * synchronise, and return 0 on success or a BB_ERR_* code; the message is
+ * cudaStream_t as `void*` (NULL = legacy default stream), never allocate (except
+ * bb_arena_alloc), never synchronise, and return 0 on success or a BB_ERR_* code; the message is
  * available from bb_last_error() (thread-local).  No C++ exception crosses
  * this boundary.
  */
