@@ -101,3 +101,31 @@ def test_project_qkv_reference_cases():
     p = Lyr.AttentionParams(2, *(seeded_random_matrix(2, 2, s) for s in (2, 3, 4)), np.eye(2))
     q, k, v = Lyr.project_qkv(np.zeros((4, 2)), p)
     assert not q.any() and not k.any() and not v.any()
+
+
+@pytest.mark.parametrize("kind", ["zigzag", "striped"])
+def test_projected_shards_feed_the_ring_kernels(kind):
+    """X -> project_qkv_shards (permutation fused into the GEMM store) -> ring forward steps on
+    the shards (all (i, j) pairs of a G=4 ring, one GPU) == attention of the projected sequence."""
+    import math
+
+    from paper_2509_19836_b200 import kernels as K
+
+    n, d, g = 2048, 128, 4
+    p = _params(d, 7)
+    x = _bf16(np.random.default_rng(8).uniform(-1, 1, (n, d)))
+    layout = ShardLayout(kind, n, g)
+    shards = Lyr.project_qkv_shards(x, p, layout)
+    dm = K.device_mask(causal_mask(), torch.device("cuda"))
+    ref_q, ref_k, ref_v = (_bf16(x @ w) for w in (p.w_q, p.w_k, p.w_v))
+    o_ref, lse_ref = O.attention_forward(ref_q, ref_k, ref_v, O.allowed(("causal", None, None, None),
+                                                                         np.arange(1, n + 1), np.arange(1, n + 1)))
+    for i in range(g):
+        qi = shards[i][0]
+        o = torch.zeros(n // g, 1, d, device="cuda")
+        lse = torch.full((1, n // g), float("-inf"), device="cuda")
+        for j in range(g):
+            K.attn_fwd_step(qi, shards[j][1], shards[j][2], o, lse, layout, dm, i + 1, j + 1, 1.0 / math.sqrt(d))
+        rows = device_token_ids(layout, i + 1) - 1
+        assert np.abs(o[:, 0].double().cpu().numpy() - o_ref[rows]).max() < 1e-2
+        assert np.abs(lse[0].double().cpu().numpy() - lse_ref[rows]).max() < 2e-3
