@@ -7,6 +7,8 @@ Three of the reference CLI's subcommands (``burstsim/cli.py:113-131``), emitting
                 backward traffic ratio (``cli.py:298-330``) — host logic, bit-identical;
 * ``balance``   per-device and per-step unmasked-pair tables (``cli.py:333-386``) —
                 host logic, bit-identical;
+* ``checkpoint`` the three checkpoint policies' storage / recompute plan (``cli.py:514-583``) —
+                host logic, bit-identical — and the toy run, executed on the GPU;
 * ``timeline``  the event timeline of one ring pass (``cli.py:389-441``) — MEASURED here:
                 the pass runs on the local GPUs through ``run_with_schedule`` (CUDA events
                 per ring step and per peer copy), where the reference simulates it.
@@ -179,6 +181,42 @@ def cmd_balance(a) -> Report:
     return rep
 
 
+def cmd_checkpoint(a) -> Report:
+    from .checkpointing import FULL_RECOMPUTE, SELECTIVE_PP, SEQUENCE_SELECTIVE, CheckpointPolicy, execute_toy
+    from .checkpointing import plan as checkpoint_plan
+
+    problems: list[str] = []
+    mask = _mask(a, a.seq, problems)
+    if a.seq > 64:
+        problems.append(f"seq: toy checkpoint runs are capped at 64 tokens, got {a.seq}")
+    if problems or mask is None:
+        raise BadConfig(problems)
+    rep = Report("checkpoint", a.seed, {"seq_len_tokens": a.seq, "dim": a.dim, "mask": mask.describe(),
+                                        "checkpoint_split": a.split})
+    rows, toy_rows = [], []
+    try:
+        for pol in (CheckpointPolicy(FULL_RECOMPUTE), CheckpointPolicy(SELECTIVE_PP),
+                    CheckpointPolicy(SEQUENCE_SELECTIVE, a.split)):
+            pr = checkpoint_plan(pol, a.seq, a.dim, mask)
+            rows.append([pol.kind, pr.stored_elements_per_layer, pr.attention_extra_elements, pr.recompute_pairs,
+                         pr.recompute_fraction])
+            if not a.no_toy:
+                import torch
+
+                if not torch.cuda.is_available():
+                    raise BadConfig(["checkpoint: the toy run executes on a CUDA device (use --no-toy for the plan)"])
+                toy = execute_toy(pol, a.seq, a.dim, mask, a.seed)
+                toy_rows.append([pol.kind, toy.recomputed_pairs, toy.max_grad_diff,
+                                 "yes" if toy.matches_baseline else "no"])
+    except ValueError as exc:
+        raise BadConfig([str(exc)]) from exc
+    rep.section("plan", ["policy", "stored_elements_per_layer", "attention_extra_elements", "recompute_pairs",
+                         "recompute_fraction"], rows)
+    if not a.no_toy:
+        rep.section("toy_run", ["policy", "recomputed_pairs", "max_grad_diff", "matches_baseline"], toy_rows)
+    return rep
+
+
 def cmd_timeline(a) -> Report:
     """One ring pass measured on the local GPUs (reference: simulated, cli.py:389-441)."""
     problems: list[str] = []
@@ -249,6 +287,18 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--block-len-tokens", type=int, default=None, dest="block_len")
     p.add_argument("--block-window-tokens", type=int, default=None, dest="block_window")
     p.set_defaults(run=cmd_balance)
+
+    p = sub.add_parser("checkpoint", help="checkpoint policy plans and toy run")
+    common(p)
+    p.add_argument("--seq", type=int, default=16)
+    p.add_argument("--dim", type=int, default=4)
+    p.add_argument("--checkpoint-split", type=float, default=0.5, dest="split")
+    p.add_argument("--mask", choices=MASK_KINDS, default="causal")
+    p.add_argument("--window-tokens", type=int, default=None, dest="window")
+    p.add_argument("--block-len-tokens", type=int, default=None, dest="block_len")
+    p.add_argument("--block-window-tokens", type=int, default=None, dest="block_window")
+    p.add_argument("--no-toy", action="store_true", help="plan only (the toy run needs a GPU)")
+    p.set_defaults(run=cmd_checkpoint)
 
     p = sub.add_parser("timeline", help="measured event timeline of one ring pass (GPU)")
     common(p)

@@ -23,6 +23,11 @@ CASES = {
                                            "--mask", "block_sparse", "--block-len-tokens", "8",
                                            "--block-window-tokens", "24"],
     "bad_comm_divisibility": ["comm", "--seq", "10", "--gpus", "4"],
+    "checkpoint_default": ["checkpoint"],
+    "checkpoint_window_64": ["checkpoint", "--seq", "64", "--dim", "8", "--mask", "sliding_window",
+                             "--window-tokens", "12", "--checkpoint-split", "0.25"],
+    "checkpoint_full_32": ["checkpoint", "--seq", "32", "--mask", "full", "--checkpoint-split", "0.75"],
+    "bad_checkpoint_cap": ["checkpoint", "--seq", "128"],
 }
 out = {}
 for name, argv in CASES.items():
