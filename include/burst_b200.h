@@ -14,6 +14,10 @@
  *   bb_lmhead_fused         lmhead.py:41-93         fused_lmhead_loss (loss, dH, dW)
  *   bb_gemm_bf16_rows       oracle.py:60-65 +       project_qkv with shard_rows' permutation
  *                           distributed.py:104-117  fused into the GEMM store
+ *   bb_matmul_f64 ...       numerics.py:35-116      the reference's float64 tile math
+ *   bb_xent_f64             oracle.py:129-154       (matmul, row_logsumexp, lse_merge,
+ *                                                   exp_shifted, exp_gap, rowsum_hadamard)
+ *                                                   and naive_lmhead_loss's softmax - onehot
  *   bb_ipc_* / bb_arena_* / fabric.py:180-226       a ring step's payload transfer (copy
  *   bb_copy_async / bb_flag_*                       engines over NVLink + stream-ordered flags)
  *
@@ -209,6 +213,26 @@ int bb_ipc_close(void* ptr);
 int bb_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
 int bb_flag_write(void* flag, uint32_t value, void* stream);
 int bb_flag_wait(const void* flag, uint32_t value, void* stream);
+
+/* ---- float64 tile math (burstsim/numerics.py, oracle.py:129-154) ----
+ * Device pointers to float64; -inf is an exact sentinel as in the reference
+ * (numerics.py:62-69,101-116).  bb_matmul_f64: C[m,n] (row-major, contiguous)
+ * = sum_k A[i*sa0 + k*sa1] * B[k*sb0 + j*sb1], k ascending (transposes are
+ * stride swaps).  bb_row_logsumexp_f64: rows of `cols` at stride `lds`, all -inf
+ * rows give -inf.  bb_lse_merge_f64: np.logaddexp.  bb_exp_shifted_f64:
+ * exp(s - lse[:,None]), rows with lse == -inf give 0.  bb_exp_gap_f64: exp(a-b),
+ * a == -inf gives 0.  bb_rowsum_hadamard_f64: out[i] = sum_j a[i,j] b[i,j].
+ * bb_xent_f64: loss[r] = lse[r] - logits[r, y_r], g = exp(logits - lse) - onehot(y)
+ * (0-based targets, checked by the caller). */
+int bb_matmul_f64(const double* a, int64_t sa0, int64_t sa1, const double* b, int64_t sb0, int64_t sb1,
+                  double* c, int64_t m, int64_t n, int64_t k, void* stream);
+int bb_row_logsumexp_f64(const double* s, int64_t rows, int64_t cols, int64_t lds, double* out, void* stream);
+int bb_lse_merge_f64(const double* a, const double* b, double* out, int64_t n, void* stream);
+int bb_exp_shifted_f64(const double* s, const double* lse, double* out, int64_t rows, int64_t cols, void* stream);
+int bb_exp_gap_f64(const double* a, const double* b, double* out, int64_t n, void* stream);
+int bb_rowsum_hadamard_f64(const double* a, const double* b, double* out, int64_t rows, int64_t cols, void* stream);
+int bb_xent_f64(const double* logits, const double* lse, const int64_t* targets, int64_t rows, int64_t vocab,
+                double* loss, double* g, void* stream);
 
 const char* bb_last_error(void);
 /* Diagnostics: with BB_PROBE=1 in the environment, kernels record per-phase

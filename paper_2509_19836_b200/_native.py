@@ -39,6 +39,13 @@ EXPORTS = (
     "bb_copy_async",
     "bb_flag_write",
     "bb_flag_wait",
+    "bb_matmul_f64",
+    "bb_row_logsumexp_f64",
+    "bb_lse_merge_f64",
+    "bb_exp_shifted_f64",
+    "bb_exp_gap_f64",
+    "bb_rowsum_hadamard_f64",
+    "bb_xent_f64",
     "bb_last_error",
     "bb_debug_probe",
     "bb_abi_version",
@@ -162,6 +169,13 @@ def load(path: os.PathLike | str | None = None) -> C.CDLL:
     lib.bb_copy_async.argtypes = [vp, vp, i64, vp]
     lib.bb_flag_write.argtypes = [vp, C.c_uint32, vp]
     lib.bb_flag_wait.argtypes = [vp, C.c_uint32, vp]
+    lib.bb_matmul_f64.argtypes = [vp, i64, i64, vp, i64, i64, vp, i64, i64, i64, vp]
+    lib.bb_row_logsumexp_f64.argtypes = [vp, i64, i64, i64, vp, vp]
+    lib.bb_lse_merge_f64.argtypes = [vp, vp, vp, i64, vp]
+    lib.bb_exp_shifted_f64.argtypes = [vp, vp, vp, i64, i64, vp]
+    lib.bb_exp_gap_f64.argtypes = [vp, vp, vp, i64, vp]
+    lib.bb_rowsum_hadamard_f64.argtypes = [vp, vp, vp, i64, i64, vp]
+    lib.bb_xent_f64.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp]
     lib.bb_last_error.restype = C.c_char_p
     lib.bb_debug_probe.argtypes = [vp, i32]
     lib.bb_abi_version.restype = i32

@@ -272,4 +272,40 @@ int bb_lmhead_fused(const bb_lmhead_args* a, void* stream) {
   return BB_OK;
 }
 
+// ---- float64 tile math (numerics.py:35-116, oracle.py:129-154) ----
+#define BB_ST static_cast<cudaStream_t>(stream)
+int bb_matmul_f64(const double* a, int64_t sa0, int64_t sa1, const double* b, int64_t sb0, int64_t sb1,
+                  double* c, int64_t m, int64_t n, int64_t k, void* stream) {
+  if ((m * k && !a) || (k * n && !b) || (m * n && !c)) return set_error(BB_ERR_INVALID, "bb_matmul_f64: null operand");
+  return launch_matmul_f64(a, sa0, sa1, b, sb0, sb1, c, m, n, k, BB_ST);
+}
+int bb_row_logsumexp_f64(const double* s, int64_t rows, int64_t cols, int64_t lds, double* out, void* stream) {
+  if (rows < 0 || cols <= 0 || lds < cols)
+    return set_error(BB_ERR_INVALID, "row_logsumexp requires a nonempty matrix (rows %lld, cols %lld, lds %lld)",
+                     (long long)rows, (long long)cols, (long long)lds);
+  return launch_row_lse_f64(s, rows, cols, lds, out, BB_ST);
+}
+int bb_lse_merge_f64(const double* a, const double* b, double* out, int64_t n, void* stream) {
+  if (n < 0) return set_error(BB_ERR_INVALID, "bb_lse_merge_f64: negative length");
+  return launch_lse_merge_f64(a, b, out, n, BB_ST);
+}
+int bb_exp_shifted_f64(const double* s, const double* lse, double* out, int64_t rows, int64_t cols, void* stream) {
+  if (rows < 0 || cols < 0) return set_error(BB_ERR_INVALID, "bb_exp_shifted_f64: negative extent");
+  return launch_exp_shifted_f64(s, lse, out, rows, cols, BB_ST);
+}
+int bb_exp_gap_f64(const double* a, const double* b, double* out, int64_t n, void* stream) {
+  if (n < 0) return set_error(BB_ERR_INVALID, "bb_exp_gap_f64: negative length");
+  return launch_exp_gap_f64(a, b, out, n, BB_ST);
+}
+int bb_rowsum_hadamard_f64(const double* a, const double* b, double* out, int64_t rows, int64_t cols, void* stream) {
+  if (rows < 0 || cols < 0) return set_error(BB_ERR_INVALID, "bb_rowsum_hadamard_f64: negative extent");
+  return launch_rowsum_hadamard_f64(a, b, out, rows, cols, BB_ST);
+}
+int bb_xent_f64(const double* logits, const double* lse, const int64_t* targets, int64_t rows, int64_t vocab,
+                double* loss, double* g, void* stream) {
+  if (rows < 0 || vocab <= 0) return set_error(BB_ERR_INVALID, "bb_xent_f64: bad extent");
+  return launch_xent_f64(logits, lse, targets, rows, vocab, loss, g, BB_ST);
+}
+#undef BB_ST
+
 }  // extern "C"

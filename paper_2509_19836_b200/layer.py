@@ -223,3 +223,76 @@ def attention_backward(q, k, v, o, lse, do, mask: MaskSpec, device=None) -> Atte
     if isinstance(q, torch.Tensor):
         return grads
     return AttentionGrads(*(t.double().cpu().numpy() for t in (grads.dq, grads.dk, grads.dv)))
+
+
+@dataclass(frozen=True)
+class LmHeadResult:
+    """oracle.py:121-126: per-token loss (nats), dH, dW."""
+
+    loss: np.ndarray
+    dh: np.ndarray
+    dw: np.ndarray
+
+
+def naive_lmhead_loss(h, w_head, targets, device=None) -> LmHeadResult:
+    """Full-materialisation LM head + cross entropy with analytic gradients (oracle.py:129-154).
+
+    Float64 end to end on the device (``numerics`` kernels): logits = H W^T, row LSE,
+    loss = lse - logit[y], dlogits = softmax - onehot(y) in one pass, dH = G W, dW = G^T H
+    (the transposes are stride swaps).  This is the float64 check of the bf16 fused head
+    (``fused_lmhead_loss``); NumPy inputs give NumPy outputs.
+    """
+    from . import numerics as F
+
+    dev = h.device if isinstance(h, torch.Tensor) and h.is_cuda else _device(device)
+    host = not (isinstance(h, torch.Tensor) and h.is_cuda)
+    ht = F._as(h, 2, "H", dev)
+    wt = F._as(w_head, 2, "W_head", dev)
+    y = targets.detach().to("cpu") if isinstance(targets, torch.Tensor) else targets
+    y = np.asarray(y, dtype=np.int64)
+    n, d = ht.shape
+    v = wt.shape[0]
+    if wt.shape[1] != d:
+        raise ValueError(f"W_head must have {d} columns, got {wt.shape[1]}")
+    if y.shape != (n,):
+        raise ValueError(f"targets must have length {n}, got shape {y.shape}")
+    bad = np.nonzero((y < 0) | (y >= v))[0]
+    if bad.size:
+        raise ValueError(f"target index {y[bad[0]]} at row {int(bad[0])} outside [0, {v})")
+    yt = torch.from_numpy(y).to(dev)
+    logits = F.matmul(ht, wt.t())
+    lse = F.row_logsumexp(logits) if n else torch.empty(0, dtype=torch.float64, device=dev)
+    loss, g = F.softmax_xent(logits, lse, yt)
+    dh = F.matmul(g, wt)
+    dw = F.matmul(g.t(), ht)
+    if host:
+        return LmHeadResult(loss=loss.cpu().numpy(), dh=dh.cpu().numpy(), dw=dw.cpu().numpy())
+    return LmHeadResult(loss=loss, dh=dh, dw=dw)
+
+
+def finite_diff_check(f, x, analytic_grad, h: float = 1e-6) -> float:
+    """oracle.py:157-187: worst relative error of central differences of ``f`` against
+    ``analytic_grad`` (denominator max(|analytic|, 1e-8) per entry).  Host-side test
+    utility: ``f`` is the caller's function and runs wherever it runs."""
+    from .numerics import as_matrix
+
+    if h <= 0:
+        raise ValueError(f"step size must be positive, got {h}")
+    x = as_matrix(x, "finite-difference point")
+    g = as_matrix(analytic_grad, "analytic gradient")
+    if g.shape != x.shape:
+        raise ValueError(f"gradient shape {g.shape} != point shape {x.shape}")
+    worst = 0.0
+    probe = x.copy()
+    for idx in np.ndindex(*x.shape):
+        centre = x[idx]
+        probe[idx] = centre + h
+        hi = float(f(probe.copy()))
+        probe[idx] = centre - h
+        lo = float(f(probe.copy()))
+        probe[idx] = centre
+        if not (math.isfinite(hi) and math.isfinite(lo)):
+            raise ValueError(f"f is non-finite near entry {idx}")
+        err = abs((hi - lo) / (2.0 * h) - g[idx]) / max(abs(g[idx]), 1e-8)
+        worst = max(worst, float(err))
+    return worst
