@@ -1,6 +1,6 @@
 """``python -m paper_2509_19836_b200`` — burstsim-compatible reports.
 
-Three of the reference CLI's subcommands (``burstsim/cli.py:113-131``), emitting the same
+Five of the reference CLI's subcommands (``burstsim/cli.py:113-131``), emitting the same
 ``schema_version = 1`` report (``reporting.py:17,90-105``) in table / csv / json:
 
 * ``comm``      per-pass element accounting, the Table-1 analytic times, the burst / ring
@@ -9,6 +9,10 @@ Three of the reference CLI's subcommands (``burstsim/cli.py:113-131``), emitting
                 host logic, bit-identical;
 * ``checkpoint`` the three checkpoint policies' storage / recompute plan (``cli.py:514-583``) —
                 host logic, bit-identical — and the toy run, executed on the GPU;
+* ``lmhead``    fused vs naive LM head (``cli.py:444-511``): the fused head runs on the
+                tcgen05 kernels (bf16 operands, fp32 accumulation), the naive head and the
+                finite-difference check in float64 on the device (``numerics``); the
+                footprint section is host logic, identical to the reference's;
 * ``timeline``  the event timeline of one ring pass (``cli.py:389-441``) — MEASURED here:
                 the pass runs on the local GPUs through ``run_with_schedule`` (CUDA events
                 per ring step and per peer copy), where the reference simulates it.
@@ -217,6 +221,46 @@ def cmd_checkpoint(a) -> Report:
     return rep
 
 
+def cmd_lmhead(a) -> Report:
+    """Fused vs naive LM head (reference: cli.py:444-511, same inputs and report sections)."""
+    from .layer import finite_diff_check, naive_lmhead_loss
+    from .lmhead import FusionConfig, fused_lmhead_loss, memory_footprint
+    from .numerics import seeded_random_matrix
+
+    if a.row_tile is None:
+        a.row_tile = max(1, a.seq // 2 if a.seq else 4)
+    if a.vocab_tile is None:
+        a.vocab_tile = max(1, (a.vocab or 17) // 3)
+    problems = [f"{name}: must be >= 1, got {getattr(a, name)}"
+                for name in ("seq", "dim", "vocab", "row_tile", "vocab_tile") if getattr(a, name) < 1]
+    if problems:
+        raise BadConfig(problems)
+    import torch
+
+    if not torch.cuda.is_available():
+        raise BadConfig(["lmhead: the fused and naive heads execute on a CUDA device (no CPU fallback)"])
+    h = seeded_random_matrix(a.seq, a.dim, a.seed)
+    w = seeded_random_matrix(a.vocab, a.dim, a.seed + 1)
+    y = np.random.default_rng(a.seed + 2).integers(0, a.vocab, size=a.seq)
+    cfg = FusionConfig(a.row_tile, a.vocab_tile)
+    naive = naive_lmhead_loss(h, w, y)
+    fused = fused_lmhead_loss(h, w, y, cfg)
+    naive_elems, fused_elems = memory_footprint(a.seq, a.vocab, a.dim, cfg)
+    fd_err = finite_diff_check(lambda x: float(np.sum(naive_lmhead_loss(x, w, y).loss)), h, naive.dh, h=1e-6)
+    rep = Report("lmhead", a.seed, {"seq_len_tokens": a.seq, "dim": a.dim, "vocab": a.vocab,
+                                    "row_tile": a.row_tile, "vocab_tile": a.vocab_tile})
+    rep.section("equivalence", ["metric", "value"], [
+        ["max_abs_loss_diff", float(np.max(np.abs(fused.loss - naive.loss)))],
+        ["max_abs_dh_diff", float(np.max(np.abs(fused.dh - naive.dh)))],
+        ["max_abs_dw_diff", float(np.max(np.abs(fused.dw - naive.dw)))],
+        ["finite_difference_rel_err", fd_err],
+        ["total_loss_nats", float(np.sum(fused.loss))],
+    ])
+    rep.section("footprint_elements", ["naive_logits", "fused_peak_model", "fused_peak_instrumented"],
+                [[naive_elems, fused_elems, fused.peak_aux_elements]])
+    return rep
+
+
 def cmd_timeline(a) -> Report:
     """One ring pass measured on the local GPUs (reference: simulated, cli.py:389-441)."""
     problems: list[str] = []
@@ -299,6 +343,15 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--block-window-tokens", type=int, default=None, dest="block_window")
     p.add_argument("--no-toy", action="store_true", help="plan only (the toy run needs a GPU)")
     p.set_defaults(run=cmd_checkpoint)
+
+    p = sub.add_parser("lmhead", help="fused vs naive LM-head loss (GPU)")
+    common(p)
+    p.add_argument("--seq", type=int, default=8)
+    p.add_argument("--dim", type=int, default=4)
+    p.add_argument("--vocab", type=int, default=17)
+    p.add_argument("--row-tile", type=int, default=None, dest="row_tile")
+    p.add_argument("--vocab-tile", type=int, default=None, dest="vocab_tile")
+    p.set_defaults(run=cmd_lmhead)
 
     p = sub.add_parser("timeline", help="measured event timeline of one ring pass (GPU)")
     common(p)

@@ -1,4 +1,4 @@
-"""Golden reports of the reference CLI (burstsim/cli.py comm / balance) for tests/test_cli.py.
+"""Golden reports of the reference CLI (burstsim/cli.py comm / balance / checkpoint / lmhead) for tests/test_cli.py.
 
 Run in the build container (reads /root/reference, read-only):
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_cli_golden.py
@@ -28,6 +28,12 @@ CASES = {
                              "--window-tokens", "12", "--checkpoint-split", "0.25"],
     "checkpoint_full_32": ["checkpoint", "--seq", "32", "--mask", "full", "--checkpoint-split", "0.75"],
     "bad_checkpoint_cap": ["checkpoint", "--seq", "128"],
+    "lmhead_default": ["lmhead"],
+    "lmhead_64_16_257": ["lmhead", "--seq", "64", "--dim", "16", "--vocab", "257", "--row-tile", "8",
+                         "--vocab-tile", "32", "--seed", "3"],
+    "lmhead_ragged_tiles": ["lmhead", "--seq", "13", "--dim", "5", "--vocab", "29", "--row-tile", "4",
+                            "--vocab-tile", "7", "--seed", "11"],
+    "bad_lmhead_sizes": ["lmhead", "--seq", "0", "--vocab-tile", "-1"],
 }
 out = {}
 for name, argv in CASES.items():

@@ -14,7 +14,8 @@ from paper_2509_19836_b200.cli import main
 GOLDEN = json.loads((Path(__file__).parent / "golden" / "cli_golden.json").read_text())
 
 
-HOST_ONLY = sorted(n for n in GOLDEN if not n.startswith("checkpoint_"))
+HOST_ONLY = sorted(n for n in GOLDEN if not n.startswith(("checkpoint_", "lmhead_")))
+LMHEAD_JSON = sorted(n for n in GOLDEN if n.startswith("lmhead_") and n.endswith("/json"))
 CHECKPOINT_JSON = sorted(n for n in GOLDEN if n.startswith("checkpoint_") and n.endswith("/json"))
 
 
@@ -91,3 +92,28 @@ def test_checkpoint_toy_run_on_the_gpu():
     assert [r[0] for r in toy["rows"]] == [r[0] for r in want_toy["rows"]]
     assert [r[1] for r in toy["rows"]] == [r[1] for r in want_toy["rows"]]  # recomputed pairs: exact
     assert all(r[3] == "yes" for r in toy["rows"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", LMHEAD_JSON)
+def test_lmhead_report_on_the_gpu(name):
+    """lmhead (cli.py:444-511): params, total loss and the footprint section as the reference
+    reports them; the fused head is bf16 on the tensor cores, so its distance from the fp64 naive
+    head is bf16-sized (the reference's is ~1e-16); the fp64 naive head's finite-difference check
+    reproduces the reference's figure."""
+    g = GOLDEN[name]
+    so = io.StringIO()
+    with contextlib.redirect_stdout(so):
+        rc = main(g["argv"])
+    assert rc == g["rc"] == 0
+    doc, want = json.loads(so.getvalue()), json.loads(g["stdout"])
+    assert doc["params"] == want["params"] and doc["command"] == want["command"] == "lmhead"
+    sec = {s["name"]: s for s in doc["sections"]}
+    ref = {s["name"]: s for s in want["sections"]}
+    assert sec["footprint_elements"] == ref["footprint_elements"]
+    got, exp = dict(sec["equivalence"]["rows"]), dict(ref["equivalence"]["rows"])
+    assert abs(got["total_loss_nats"] - exp["total_loss_nats"]) <= 2e-3 * max(1.0, abs(exp["total_loss_nats"]))
+    for key in ("max_abs_loss_diff", "max_abs_dh_diff", "max_abs_dw_diff"):
+        assert got[key] < 3e-2, key
+    # the fp64 naive head's finite-difference figure is the reference's own (measured: 7.5e-9 apart)
+    assert abs(got["finite_difference_rel_err"] - exp["finite_difference_rel_err"]) <= 1e-4 * exp["finite_difference_rel_err"] + 1e-9
