@@ -1,6 +1,6 @@
 """``python -m paper_2509_19836_b200`` — burstsim-compatible reports.
 
-Five of the reference CLI's subcommands (``burstsim/cli.py:113-131``), emitting the same
+Six of the reference CLI's subcommands (``burstsim/cli.py:113-131``), emitting the same
 ``schema_version = 1`` report (``reporting.py:17,90-105``) in table / csv / json:
 
 * ``comm``      per-pass element accounting, the Table-1 analytic times, the burst / ring
@@ -9,6 +9,9 @@ Five of the reference CLI's subcommands (``burstsim/cli.py:113-131``), emitting 
                 host logic, bit-identical;
 * ``checkpoint`` the three checkpoint policies' storage / recompute plan (``cli.py:514-583``) —
                 host logic, bit-identical — and the toy run, executed on the GPU;
+* ``verify``    the property battery (``cli.py:282-295``, ``verification.py``) against the
+                GPU engine (``verification.py`` here: host checks exact, device checks at
+                the build tolerances);
 * ``lmhead``    fused vs naive LM head (``cli.py:444-511``): the fused head runs on the
                 tcgen05 kernels (bf16 operands, fp32 accumulation), the naive head and the
                 finite-difference check in float64 on the device (``numerics``); the
@@ -49,7 +52,7 @@ from .masks import MASK_KINDS, causal_mask, full_mask, sliding_window_mask, vali
 from .partitioning import LAYOUT_KINDS, ShardLayout, balance_report, block_mask_from_window
 
 SCHEMA_VERSION = 1
-EXIT_OK, EXIT_BAD_CONFIG = 0, 2
+EXIT_OK, EXIT_SUITE_FAILED, EXIT_BAD_CONFIG = 0, 1, 2
 
 
 class BadConfig(Exception):
@@ -221,6 +224,24 @@ def cmd_checkpoint(a) -> Report:
     return rep
 
 
+def cmd_verify(a) -> Report:
+    """The property battery (reference: cli.py:282-295) on the B200 engine (``verification``)."""
+    import torch
+
+    from .verification import run_all
+
+    if not torch.cuda.is_available():
+        raise BadConfig(["verify: the property suite executes on a CUDA device (no CPU fallback)"])
+    checks = run_all(a.seed)
+    failed = sum(not c.passed for c in checks)
+    rep = Report("verify", a.seed, {})
+    rep.section("checks", ["check", "status", "detail"], [[c.name, "PASS" if c.passed else "FAIL", c.detail]
+                                                           for c in checks])
+    rep.section("summary", ["total", "passed", "failed"], [[len(checks), len(checks) - failed, failed]])
+    rep.exit_code = EXIT_SUITE_FAILED if failed else EXIT_OK
+    return rep
+
+
 def cmd_lmhead(a) -> Report:
     """Fused vs naive LM head (reference: cli.py:444-511, same inputs and report sections)."""
     from .layer import finite_diff_check, naive_lmhead_loss
@@ -314,6 +335,10 @@ def build_parser() -> argparse.ArgumentParser:
         p.add_argument("--bw-intra-elements-per-s", type=float, default=1e9, dest="bw_intra")
         p.add_argument("--bw-inter-elements-per-s", type=float, default=1e8, dest="bw_inter")
 
+    p = sub.add_parser("verify", help="run the property suite on the GPU engine")
+    common(p)
+    p.set_defaults(run=cmd_verify)
+
     p = sub.add_parser("comm", help="traffic accounting and analytic times")
     common(p)
     p.add_argument("--seq", type=int, default=8)
@@ -378,4 +403,4 @@ def main(argv=None) -> int:
         Path(args.output).write_text(text)
     else:
         sys.stdout.write(text)
-    return EXIT_OK
+    return getattr(rep, "exit_code", EXIT_OK)

@@ -34,6 +34,7 @@ CASES = {
     "lmhead_ragged_tiles": ["lmhead", "--seq", "13", "--dim", "5", "--vocab", "29", "--row-tile", "4",
                             "--vocab-tile", "7", "--seed", "11"],
     "bad_lmhead_sizes": ["lmhead", "--seq", "0", "--vocab-tile", "-1"],
+    "verify_default": ["verify"],
 }
 out = {}
 for name, argv in CASES.items():

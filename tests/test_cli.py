@@ -14,7 +14,7 @@ from paper_2509_19836_b200.cli import main
 GOLDEN = json.loads((Path(__file__).parent / "golden" / "cli_golden.json").read_text())
 
 
-HOST_ONLY = sorted(n for n in GOLDEN if not n.startswith(("checkpoint_", "lmhead_")))
+HOST_ONLY = sorted(n for n in GOLDEN if not n.startswith(("checkpoint_", "lmhead_", "verify_")))
 LMHEAD_JSON = sorted(n for n in GOLDEN if n.startswith("lmhead_") and n.endswith("/json"))
 CHECKPOINT_JSON = sorted(n for n in GOLDEN if n.startswith("checkpoint_") and n.endswith("/json"))
 
@@ -117,3 +117,20 @@ def test_lmhead_report_on_the_gpu(name):
         assert got[key] < 3e-2, key
     # the fp64 naive head's finite-difference figure is the reference's own (measured: 7.5e-9 apart)
     assert abs(got["finite_difference_rel_err"] - exp["finite_difference_rel_err"]) <= 1e-4 * exp["finite_difference_rel_err"] + 1e-9
+
+
+@pytest.mark.gpu
+def test_verify_battery_on_the_gpu():
+    """verify (cli.py:282-295): every check of the battery passes on the GPU engine (exit 0);
+    the check names are the reference's, minus its simulator / cost-model checks."""
+    so = io.StringIO()
+    with contextlib.redirect_stdout(so):
+        rc = main(["verify", "--format", "json"])
+    doc = json.loads(so.getvalue())
+    rows = {s["name"]: s for s in doc["sections"]}["checks"]["rows"]
+    assert rc == 0, [r for r in rows if r[1] != "PASS"]
+    want = json.loads(GOLDEN["verify_default/json"]["stdout"])
+    ref_names = [r[0] for r in {s["name"]: s for s in want["sections"]}["checks"]["rows"]]
+    names = [r[0] for r in rows]
+    assert set(names) <= set(ref_names) and len(names) == len(ref_names) - 6
+    assert all(r[1] == "PASS" for r in rows)
