@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include <algorithm>
+
 #include "bb_host.h"
 
 namespace bb {
@@ -73,11 +75,12 @@ __global__ void lse_merge_kernel(const double* __restrict__ a, const double* __r
 
 __global__ void exp_shifted_kernel(const double* __restrict__ s, const double* __restrict__ lse,
                                    double* __restrict__ out, int64_t rows, int64_t cols) {
-  const int64_t r = blockIdx.y;
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r >= rows || c >= cols) return;
-  const double l = lse[r];
-  out[r * cols + c] = (l == -CUDART_INF) ? 0.0 : exp(s[r * cols + c] - l);
+  const int64_t total = rows * cols;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double l = lse[i / cols];
+    out[i] = (l == -CUDART_INF) ? 0.0 : exp(s[i] - l);
+  }
 }
 
 __global__ void exp_gap_kernel(const double* __restrict__ a, const double* __restrict__ b,
@@ -202,9 +205,8 @@ int launch_lse_merge_f64(const double* a, const double* b, double* out, int64_t 
 int launch_exp_shifted_f64(const double* s, const double* lse, double* out, int64_t rows, int64_t cols,
                            cudaStream_t st) {
   if (rows == 0 || cols == 0) return BB_OK;
-  if (rows > 65535) return set_error(BB_ERR_UNSUPPORTED, "bb_exp_shifted_f64: rows %lld > 65535", (long long)rows);
-  dim3 grid(blocks_for(cols, 256), static_cast<unsigned>(rows));
-  exp_shifted_kernel<<<grid, 256, 0, st>>>(s, lse, out, rows, cols);
+  const int64_t blocks = std::min<int64_t>((rows * cols + 255) / 256, int64_t(num_sms()) * 16);
+  exp_shifted_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(s, lse, out, rows, cols);
   return check_launch("exp_shifted_kernel");
 }
 

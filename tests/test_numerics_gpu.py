@@ -137,3 +137,13 @@ def test_naive_lmhead_finite_difference(cuda):
     res = Lyr.naive_lmhead_loss(h, w, y)
     assert Lyr.finite_diff_check(lambda x: Lyr.naive_lmhead_loss(x, w, y).loss.sum(), h, res.dh) < 1e-5
     assert Lyr.finite_diff_check(lambda x: Lyr.naive_lmhead_loss(h, x, y).loss.sum(), w, res.dw) < 1e-5
+
+
+def test_exp_shifted_many_rows(cuda):
+    # more rows than a CUDA grid's y extent: the kernel walks rows x cols flat
+    s = O.seeded_random_matrix(70001, 3, 12)
+    lse = O.lse_rows(s)
+    lse[70000] = -INF
+    out = F.exp_shifted(s, lse)
+    assert np.all(out[70000] == 0.0)
+    _close(out, O.exp_shifted(s, lse), 1e-14)
