@@ -402,18 +402,26 @@ def run_gpu(args) -> None:
         def run_e2e(steps: int, start_evt=None, end_evt=None):
             if start_evt is not None:
                 start_evt.record(stream)
-            up = [torch.cuda.Event(), torch.cuda.Event()]
+            up = [torch.cuda.Event(), torch.cuda.Event()]  # Q, K, V uploaded (the forward's inputs)
+            up_do = [torch.cuda.Event(), torch.cuda.Event()]  # dO uploaded (needed by the backward only)
             done = [torch.cuda.Event(), torch.cuda.Event()]
+
+            def upload(b):
+                for dst, src in zip(dbufs[b][:3], hosts[:3]):
+                    dst.copy_(src, non_blocking=True)
+                up[b].record(copy)
+                dbufs[b][3].copy_(hosts[3], non_blocking=True)
+                up_do[b].record(copy)
+
             copy.wait_stream(stream)
             with torch.cuda.stream(copy):
-                for dst, src in zip(dbufs[0], hosts):
-                    dst.copy_(src, non_blocking=True)
-                up[0].record(copy)
+                upload(0)
             for i in range(steps):
                 b = i % 2
                 stream.wait_event(up[b])
                 x = dbufs[b]
                 ring.forward(x[0], x[1], x[2], o, lse)
+                stream.wait_event(up_do[b])
                 ring.backward(x[0], x[1], x[2], x[3], o, lse, kind=args.backward, dq=dq, dk=dk, dv=dv)
                 for dst, src in zip(gbufs[b], (dq, dk, dv)):
                     dst.copy_(src)
@@ -422,9 +430,7 @@ def run_gpu(args) -> None:
                     if i + 1 < steps:  # next step's inputs (its buffer was freed by step i-1)
                         if i >= 1:
                             copy.wait_event(done[1 - b])
-                        for dst, src in zip(dbufs[1 - b], hosts):
-                            dst.copy_(src, non_blocking=True)
-                        up[1 - b].record(copy)
+                        upload(1 - b)
                     copy.wait_event(done[b])
                     for dst, src in zip(outs[b], gbufs[b]):
                         dst.copy_(src, non_blocking=True)
@@ -447,7 +453,7 @@ def run_gpu(args) -> None:
             "unit": "TFLOPS",
             "h2d_bytes_per_step": h2d * world,
             "d2h_bytes_per_step": d2h * world,
-            "pipelining": "H2D of step i+1 and D2H of step i on a side stream, overlapping step i",
+            "pipelining": "H2D of step i+1 and D2H of step i on a side stream, overlapping step i; the forward starts once Q/K/V are up (dO lands during it)",
         }
 
     if rank != 0:
