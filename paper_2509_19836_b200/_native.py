@@ -40,6 +40,7 @@ EXPORTS = (
     "bb_flag_write",
     "bb_flag_wait",
     "bb_matmul_f64",
+    "bb_scale_mask_f64",
     "bb_row_logsumexp_f64",
     "bb_lse_merge_f64",
     "bb_exp_shifted_f64",
@@ -170,6 +171,7 @@ def load(path: os.PathLike | str | None = None) -> C.CDLL:
     lib.bb_flag_write.argtypes = [vp, C.c_uint32, vp]
     lib.bb_flag_wait.argtypes = [vp, C.c_uint32, vp]
     lib.bb_matmul_f64.argtypes = [vp, i64, i64, vp, i64, i64, vp, i64, i64, i64, vp]
+    lib.bb_scale_mask_f64.argtypes = [vp, vp, C.c_double, i64, vp]
     lib.bb_row_logsumexp_f64.argtypes = [vp, i64, i64, i64, vp, vp]
     lib.bb_lse_merge_f64.argtypes = [vp, vp, vp, i64, vp]
     lib.bb_exp_shifted_f64.argtypes = [vp, vp, vp, i64, i64, vp]

@@ -279,6 +279,10 @@ int bb_matmul_f64(const double* a, int64_t sa0, int64_t sa1, const double* b, in
   if ((m * k && !a) || (k * n && !b) || (m * n && !c)) return set_error(BB_ERR_INVALID, "bb_matmul_f64: null operand");
   return launch_matmul_f64(a, sa0, sa1, b, sb0, sb1, c, m, n, k, BB_ST);
 }
+int bb_scale_mask_f64(double* s, const uint8_t* allowed, double scale, int64_t n, void* stream) {
+  if (n < 0) return set_error(BB_ERR_INVALID, "bb_scale_mask_f64: negative length");
+  return launch_scale_mask_f64(s, allowed, scale, n, BB_ST);
+}
 int bb_row_logsumexp_f64(const double* s, int64_t rows, int64_t cols, int64_t lds, double* out, void* stream) {
   if (rows < 0 || cols <= 0 || lds < cols)
     return set_error(BB_ERR_INVALID, "row_logsumexp requires a nonempty matrix (rows %lld, cols %lld, lds %lld)",

@@ -55,6 +55,7 @@ int launch_attn_bwd(const bb_attn_bwd_args& a, cudaStream_t stream);
 
 int launch_matmul_f64(const double* a, int64_t sa0, int64_t sa1, const double* b, int64_t sb0, int64_t sb1,
                       double* c, int64_t m, int64_t n, int64_t k, cudaStream_t st);
+int launch_scale_mask_f64(double* s, const uint8_t* allowed, double scale, int64_t n, cudaStream_t st);
 int launch_row_lse_f64(const double* s, int64_t rows, int64_t cols, int64_t lds, double* out, cudaStream_t st);
 int launch_lse_merge_f64(const double* a, const double* b, double* out, int64_t n, cudaStream_t st);
 int launch_exp_shifted_f64(const double* s, const double* lse, double* out, int64_t rows, int64_t cols,

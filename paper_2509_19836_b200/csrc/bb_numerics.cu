@@ -8,11 +8,14 @@
 //   exp_shifted_f64   numerics.py:101-107 exp(s - lse[:, None]); lse == -inf rows give 0
 //   exp_gap_f64       numerics.py:110-116 exp(a - b); a == -inf gives 0
 //   rowsum_hadamard   numerics.py:86-92   out[i] = sum_j a[i,j] b[i,j]
+//   scale_mask_f64    oracle.py:66-75     masked_scores: S * scale, masked entries -inf
 //   xent_f64          oracle.py:129-154   loss = lse - logit[y], g = softmax - onehot(y)
 // All are HBM-bound (one read of each operand, one write) except matmul, which runs on the
 // FP64 pipe with a 64x64 CTA tile staged in shared memory.
 #include <cuda_runtime.h>
 #include <math_constants.h>
+
+#include <algorithm>
 
 #include <algorithm>
 
@@ -120,6 +123,14 @@ __global__ void xent_kernel(const double* __restrict__ logits, const double* __r
   if (lane == 0) loss[r] = -row[y] + l;
 }
 
+// s[i] = allowed[i] ? s[i] * scale : -inf, in place (oracle.py:73-75 after the Q K^T product).
+__global__ void scale_mask_kernel(double* __restrict__ s, const uint8_t* __restrict__ allowed, double scale,
+                                  int64_t n) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    s[i] = allowed[i] ? s[i] * scale : -CUDART_INF;
+}
+
 // C[m, n] = sum_k A[m, k] B[k, n] in float64, k ascending for every element.
 // 64x64 output tile per 256-thread CTA, 4x4 per thread, K staged 16 at a time.
 constexpr int kTm = 64, kTn = 64, kTk = 16;
@@ -188,6 +199,13 @@ int launch_matmul_f64(const double* a, int64_t sa0, int64_t sa1, const double* b
   dim3 grid(blocks_for(n, kTn), blocks_for(m, kTm));
   matmul_f64_kernel<<<grid, 256, 0, st>>>(a, sa0, sa1, b, sb0, sb1, c, m, n, k);
   return check_launch("matmul_f64_kernel");
+}
+
+int launch_scale_mask_f64(double* s, const uint8_t* allowed, double scale, int64_t n, cudaStream_t st) {
+  if (n == 0) return BB_OK;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 16);
+  scale_mask_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(s, allowed, scale, n);
+  return check_launch("scale_mask_kernel");
 }
 
 int launch_row_lse_f64(const double* s, int64_t rows, int64_t cols, int64_t lds, double* out, cudaStream_t st) {

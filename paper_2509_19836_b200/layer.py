@@ -165,6 +165,26 @@ def _first_empty_row(mask: MaskSpec, nq: int, nk: int) -> int | None:
     return None
 
 
+def masked_scores(q, k, mask: MaskSpec, device=None):
+    """S = Q K^T / sqrt(d) with masked-out entries -inf (oracle.py:66-75), float64 on the device:
+    the fp64 GEMM with K^T as a stride swap, then one pass that scales and applies the
+    reference's dense allowed-pair matrix (``dense_mask``, host logic as in the reference)."""
+    from . import numerics as F
+    from .masks import dense_mask
+
+    dev = q.device if isinstance(q, torch.Tensor) and q.is_cuda else _device(device)
+    host = not (isinstance(q, torch.Tensor) and q.is_cuda)
+    qt, kt = F._as(q, 2, "Q", dev), F._as(k, 2, "K", dev)
+    if qt.shape[1] != kt.shape[1]:
+        raise ValueError(f"Q has dim {qt.shape[1]} but K has dim {kt.shape[1]}")
+    validate_mask(mask, max(qt.shape[0], kt.shape[0]))
+    s = F.matmul(qt, kt.t())
+    allowed = torch.from_numpy(np.ascontiguousarray(dense_mask(mask, qt.shape[0], kt.shape[0]), dtype=np.uint8)).to(dev)
+    N.check(N.load().bb_scale_mask_f64(s.data_ptr(), allowed.data_ptr(), 1.0 / math.sqrt(qt.shape[1]), s.numel(),
+                                       C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+    return s.cpu().numpy() if host else s
+
+
 def attention_forward(q, k, v, mask: MaskSpec, device=None) -> AttentionResult:
     """O = softmax(Q K^T / sqrt(d)) V and the row LSE (oracle.py:80-95), one device."""
     q, k, v = _matrix(q, "Q"), _matrix(k, "K"), _matrix(v, "V")

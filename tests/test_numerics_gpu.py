@@ -147,3 +147,17 @@ def test_exp_shifted_many_rows(cuda):
     out = F.exp_shifted(s, lse)
     assert np.all(out[70000] == 0.0)
     _close(out, O.exp_shifted(s, lse), 1e-14)
+
+
+def test_masked_scores_matches_reference_algorithm(cuda):
+    # oracle.py:66-75: S = Q K^T / sqrt(d), masked entries exactly -inf
+    from paper_2509_19836_b200.masks import causal_mask, dense_mask, sliding_window_mask
+
+    q, k = O.seeded_random_matrix(12, 5, 30), O.seeded_random_matrix(12, 5, 31)
+    for mask in (causal_mask(), sliding_window_mask(3)):
+        s = Lyr.masked_scores(q, k, mask)
+        allowed = dense_mask(mask, 12, 12)
+        want = np.where(allowed, O.mm(q, k.T) / np.sqrt(5), -INF)
+        _close(s, want, 1e-14)
+    with pytest.raises(ValueError, match="dim"):
+        Lyr.masked_scores(q, k[:, :3], causal_mask())
