@@ -226,8 +226,9 @@ int bb_flag_wait(const void* flag, uint32_t value, void* stream);
  * (0-based targets, checked by the caller). */
 int bb_matmul_f64(const double* a, int64_t sa0, int64_t sa1, const double* b, int64_t sb0, int64_t sb1,
                   double* c, int64_t m, int64_t n, int64_t k, void* stream);
-/* In place: s[i] = allowed[i] ? s[i] * scale : -inf (masked_scores, oracle.py:66-75). */
-int bb_scale_mask_f64(double* s, const uint8_t* allowed, double scale, int64_t n, void* stream);
+/* In place: s[i] = allowed[i] ? s[i] / root : -inf (masked_scores, oracle.py:66-75; root = sqrt(d),
+ * divided like the reference's `/ np.sqrt(d)`). */
+int bb_scale_mask_f64(double* s, const uint8_t* allowed, double root, int64_t n, void* stream);
 int bb_row_logsumexp_f64(const double* s, int64_t rows, int64_t cols, int64_t lds, double* out, void* stream);
 int bb_lse_merge_f64(const double* a, const double* b, double* out, int64_t n, void* stream);
 int bb_exp_shifted_f64(const double* s, const double* lse, double* out, int64_t rows, int64_t cols, void* stream);

@@ -55,14 +55,19 @@ def up_to_date() -> bool:
     return all(p.stat().st_mtime <= t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) -> Path:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False, defines: tuple[str, ...] = (),
+          out: Path | None = None) -> Path:
+    """Compile csrc/ into LIB.  ``defines`` (e.g. ``("BB_EXP_X",)``) and ``out`` build a
+    developer variant library elsewhere (tools/variant.py); the product build takes neither."""
+    lib = Path(out) if out else LIB
+    if not force and not defines and out is None and up_to_date():
         return LIB
-    OUT_DIR.mkdir(exist_ok=True)
-    obj_dir = OUT_DIR / "obj"
+    out_dir = lib.parent
+    out_dir.mkdir(parents=True, exist_ok=True)
+    obj_dir = out_dir / ("obj" if out is None else lib.stem + "_obj")
     obj_dir.mkdir(exist_ok=True)
     exe = nvcc()
-    extra = ["-Xptxas", "-v"] if ptxas_info else []
+    extra = (["-Xptxas", "-v"] if ptxas_info else []) + [f"-D{d}" for d in defines]
 
     def compile_one(src: Path) -> Path:
         obj = obj_dir / (src.stem + ".o")
@@ -78,13 +83,13 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(compile_one, _sources()))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [exe, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

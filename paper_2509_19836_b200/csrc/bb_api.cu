@@ -55,7 +55,7 @@ bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner, uint6
 }
 
 bool make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype, uint64_t inner, uint64_t outer,
-                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
+                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swizzle) {
   auto fn = encode_fn();
   if (!fn) {
     set_error(BB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
@@ -71,7 +71,7 @@ bool make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype,
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estride[2] = {1, 1};
   CUresult r = fn(map, dtype, 2, const_cast<void*>(base), dims, strides, box,
-                  estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  estride, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error(BB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): dims %llu x %llu, stride %llu, box %u x %u",
@@ -118,14 +118,33 @@ static int validate_ring_step(const bb_layout& L, const bb_mask& M, int64_t n_q,
     return set_error(BB_ERR_INVALID, "%s: device indices must lie in [1, %d], got i=%d, j=%d", who, L.devices, qdev, kdev);
   if (L.kind < 0 || L.kind > 3) return set_error(BB_ERR_INVALID, "%s: unknown layout kind %d", who, L.kind);
   if (M.kind < 0 || M.kind > 3) return set_error(BB_ERR_INVALID, "%s: unknown mask kind %d", who, M.kind);
+  // ShardLayout's divisibility rules (partitioning.py:53-72): every device id the kernels
+  // evaluate (token_id) must come from a valid layout, or the closed forms divide by zero.
+  if (L.seq_len < 1 || L.seq_len % L.devices)
+    return set_error(BB_ERR_INVALID, "%s: sequence length %lld must be divisible by %d devices", who,
+                     (long long)L.seq_len, L.devices);
+  if (L.kind == BB_LAYOUT_ZIGZAG && L.seq_len % (2 * static_cast<int64_t>(L.devices)))
+    return set_error(BB_ERR_INVALID, "%s: zigzag layout needs seq_len divisible by 2*devices", who);
+  if (L.kind == BB_LAYOUT_BLOCK_STRIPED &&
+      (L.block_len < 1 || L.block_len % L.devices || L.seq_len % L.block_len))
+    return set_error(BB_ERR_INVALID,
+                     "%s: block_striped layout needs block_len (%lld) > 0, divisible by %d devices, dividing seq_len %lld",
+                     who, (long long)L.block_len, L.devices, (long long)L.seq_len);
   if (M.kind == BB_MASK_BLOCK_SPARSE && (!M.block_mask || M.block_len < 1))
     return set_error(BB_ERR_INVALID, "%s: block_sparse mask needs block_mask and block_len", who);
+  // masks.py:78-86: the block mask must tile the whole sequence (the kernels index it by the
+  // block of every global id in [1, N]).
+  if (M.kind == BB_MASK_BLOCK_SPARSE && M.num_blocks * M.block_len != L.seq_len)
+    return set_error(BB_ERR_INVALID, "%s: block mask of %lld blocks x %lld does not cover seq_len %lld", who,
+                     (long long)M.num_blocks, (long long)M.block_len, (long long)L.seq_len);
   if (M.kind == BB_MASK_SLIDING_WINDOW && M.window < 1)
     return set_error(BB_ERR_INVALID, "%s: sliding_window width must be >= 1", who);
-  // Query rows are local rows [0, n_q) of device q_device; n_q < N/G is how the
-  // sequence-selective recompute runs only the front rows (checkpointing.py:149-157).
-  if (L.seq_len % L.devices || n_q > L.seq_len / L.devices || n_k != L.seq_len / L.devices)
-    return set_error(BB_ERR_INVALID, "%s: shard sizes (%lld, %lld) do not match N/G = %lld/%d", who,
+  // Query rows are local rows [0, n_q) of device q_device, key rows [0, n_k) of k_device.
+  // n_q < N/G is how the sequence-selective recompute runs only the front rows
+  // (checkpointing.py:149-157); n_q, n_k < N/G together are how a single-device layer call
+  // with nq != nk (oracle.py:80-119) runs on one shard of max(nq, nk) ids.
+  if (n_q > L.seq_len / L.devices || n_k > L.seq_len / L.devices)
+    return set_error(BB_ERR_INVALID, "%s: shard sizes (%lld, %lld) exceed N/G = %lld/%d", who,
                      (long long)n_q, (long long)n_k, (long long)L.seq_len, L.devices);
   return BB_OK;
 }

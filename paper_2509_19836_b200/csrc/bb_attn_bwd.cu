@@ -12,18 +12,27 @@
 // CTA = one 128-key tile x one kv head, K/V-stationary (the BurstAttention
 // backward's own data flow), sweeping every (query head of the GQA group,
 // 128-row query tile) the mask does not fully hide.
-//   warp 0      TMA: K, V once; Q_i (2 stages) and dO_i per query tile
-//   warp 1      MMA: S^T = K Q^T, dP^T = V dO^T          (SS, M = keys)
+//   warp 0      TMA: K, V once; Q (2 stages) and dO per query tile
+//   warp 1      MMA: S^T = K Q^T, dP^T = V dO^T          (SS, M = keys, N = 128 queries)
 //                    dV += P^T dO   with P^T read from TMEM (TS, no smem round trip)
-//                    dK += dS^T Q, dQ = dS K               (SS; dS^T read MN-major)
+//                    dK += dS^T Q   with dS^T read from TMEM (TS, over its own dP^T columns)
+//                    dQ = dS K                          (SS; dS^T read MN-major from smem)
 //   warp 2      TMEM allocator
 //   warps 4-11  two groups of 4 warps, each owning half of the 128 query columns
 //               (group g: TMEM columns of its half, all 128 lanes):
-//               P^T -> TMEM (bf16, in place over S^T), dS^T -> SWIZZLE_128B smem,
+//               P^T -> TMEM (bf16, in place over S^T), dS^T -> TMEM (over dP^T) and
+//               SWIZZLE_128B smem,
 //               final dK / dV read-modify-write.
-//   warps 12-15 dQ drain: dQ tile -> swizzled smem staging -> TMA bulk reduce-add (fp32)
-//               into the circulating dQ, overlapped with the next tile's P / dS.
+//   warps 12-15 dQ drain: the whole dQ tile TMEM -> registers at once (releasing its
+//               columns for the next dP^T), then 32-column chunks through two 16 KB smem
+//               staging slots into TMA bulk reduce-adds (fp32) on the circulating dQ.
 // TMEM: S^T / P^T [0,128), dP^T then dQ [128,256), dV [256,256+D), dK [256+D,256+2D).
+//
+// Throughput bound (tools/ubench_reduce.cu): a TMA reduce-add moves ~22.6 B/clk per SM
+// with every SM busy (L2-bound chip-wide), so the 64 KB dQ tile of D = 128 needs ~2.9k
+// cycles against 2.56k of tensor work: the drain must never idle, and the MMA chain must
+// never wait on the drain.  Registers are rebalanced with setmaxnreg so the drain warps can
+// hold a full dQ row (128 fp32) and hand its TMEM columns back in one go.
 #include <cuda_runtime.h>
 
 #include <type_traits>
@@ -35,23 +44,17 @@
 namespace bb {
 namespace {
 
-#ifndef BB_BWD_NG
-#define BB_BWD_NG 2
-#endif
-constexpr int NG = BB_BWD_NG;
-#ifndef BB_BWD_MC
-#define BB_BWD_MC 0  // 2-CTA Q/dO multicast clusters: correct since the empty-range fix, but a wash (976 vs 968 full 32K, 952 vs 955 causal 128K)
-#endif
-constexpr bool MC = BB_BWD_MC;
-#ifndef BB_BWD_DQ128
-#define BB_BWD_DQ128 1
-#endif
-              // compute column groups (4 warps each)
+constexpr int NG = 2;                      // compute column groups (4 warps each)
 constexpr int CPG = 128 / NG;              // query columns per group
 constexpr int CH = CPG / 32;               // 32-column chunks per group
 constexpr int NCOMP = NG * 128;            // compute threads
 constexpr int BWD_THREADS = 128 + NCOMP + 128;  // control warps + compute + dQ drain
 constexpr int MAX_QT = 4096;  // query tiles per shard the class table holds (n_q <= 524288)
+// setmaxnreg budget (65536 registers for 512 threads): control 72, compute 144, drain 152
+// (no spills at D = 128; a spill here reads local memory through an L1 that the 226 KB of
+// shared memory leaves at ~2 KB, i.e. from L2).
+constexpr uint32_t REGS_CTRL = 72, REGS_COMP = 144, REGS_DRAIN = 152;
+static_assert(REGS_CTRL * 128 + REGS_COMP * NCOMP + REGS_DRAIN * 128 <= 65536, "register budget");
 
 template <int D>
 struct BwdSmem {
@@ -61,9 +64,9 @@ struct BwdSmem {
   static constexpr uint32_t Q_OFF = V_OFF + TILE;    // 2 stages
   static constexpr uint32_t DO_OFF = Q_OFF + 2 * TILE;
   static constexpr uint32_t DS_OFF = DO_OFF + TILE;  // dS^T, 128 keys x 128 queries bf16
-  static constexpr uint32_t STG_OFF = DS_OFF + 128 * 128 * 2;  // 2 x [128 x 32] fp32 dQ staging
-  static constexpr uint32_t VEC_OFF = STG_OFF + 2 * 16384;     // [lse2 128 | delta 128]
-  static constexpr uint32_t BAR_OFF = VEC_OFF + 256 * 4;
+  static constexpr uint32_t STG_OFF = DS_OFF + 128 * 128 * 2;  // 2 slots x [128 x 32] fp32 dQ staging
+  static constexpr uint32_t VEC_OFF = STG_OFF + 2 * 16384;     // per column group: [lse2 64 | -D 64]
+  static constexpr uint32_t BAR_OFF = VEC_OFF + NG * 512;
   static constexpr uint32_t CLS_OFF = BAR_OFF + 256;  // 2-bit tile class per query tile
   static constexpr uint32_t BYTES = CLS_OFF + MAX_QT / 4;
 };
@@ -99,7 +102,7 @@ template <int D>
 __global__ void __launch_bounds__(BWD_THREADS, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                     const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
-                    const __grid_constant__ CUtensorMap tdq, const BwdParams p) {
+                    const __grid_constant__ CUtensorMap tdq, const __grid_constant__ BwdParams p) {
   using L = BwdSmem<D>;
   constexpr int PANELS = D / 64;
   constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 256 + D;
@@ -116,49 +119,19 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint64_t* dp_full = bars + 9;
   uint64_t* ds_full = bars + 10;
   uint64_t* dq_full = bars + 11;
-  uint64_t* dq_free = bars + 12;
+  uint64_t* dq_free = bars + 12;  // the drain has read the whole dQ tile: its columns take dP^T
   uint64_t* acc_full = bars + 13;
-  // The dP^T / dQ columns are handed over in two 64-column halves: dQ half h (head dims
-  // [64h, 64h+64)) and dP^T half g (query columns of compute group g) share TMEM columns
-  // COL_DP + 64h, so dP_g(t+1) goes as soon as the drain has read dQ half g of tile t.
-  //   dp_full[g] = bars 9 / 14, dq_full[h] = bars 11 / 15, dq_free[h] = bars 12 / 16
-  uint64_t* dp_full2[2] = {bars + 9, bars + 14};
-  uint64_t* dq_full2[2] = {bars + 11, bars + 15};
-  uint64_t* dq_free2[2] = {bars + 12, bars + 16};
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
-  float* vec_s = reinterpret_cast<float*>(smem + L::VEC_OFF);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
 
   const int kv_head = p.kv_head0 + static_cast<int>(blockIdx.y);
   const int group = p.hq / p.hkv;
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 128;  // low key tiles carry the most work
-  // MC: clusters of two adjacent key tiles share every Q / dO tile through a TMA multicast
-  // (half the L2 reads); both CTAs walk the union of their query ranges, and a query tile
-  // only one of them can see is computed by the other fully masked (P = 0).
-  const uint32_t crank = MC ? cluster_ctarank() : 0;
-  const int64_t c0p = c0 + (crank ? -128 : 128);  // the partner's key tile (MC)
-  auto q_range = [&](int64_t kc, int64_t& lo, int64_t& hi) {
-    lo = hi = 0;
-    if (kc < 0 || kc >= p.n_k) return;
-    active_runs(p.layout, p.mask, token_id(p.layout, p.k_device, kc),
-                token_id(p.layout, p.k_device, min(kc + 128, p.n_k) - 1), p.q_device, p.n_q, false, lo, hi);
-  };
   // Query tiles that can touch this key tile (two binary searches, every thread), then the
   // work items (query head of the GQA group, query tile in [q_lo, q_hi)).
-  int64_t q_lo, q_hi;
-  q_range(c0, q_lo, q_hi);
-  if (MC) {
-    int64_t p_lo, p_hi;
-    q_range(c0p, p_lo, p_hi);
-    if (p_hi > p_lo) {
-      if (q_hi > q_lo) {
-        q_lo = min(q_lo, p_lo);
-        q_hi = max(q_hi, p_hi);
-      } else {
-        q_lo = p_lo;
-        q_hi = p_hi;
-      }
-    }
-  }
+  int64_t q_lo = 0, q_hi = 0;
+  if (c0 < p.n_k)
+    active_runs(p.layout, p.mask, token_id(p.layout, p.k_device, c0),
+                token_id(p.layout, p.k_device, min(c0 + 128, p.n_k) - 1), p.q_device, p.n_q, false, q_lo, q_hi);
   const uint32_t nr = static_cast<uint32_t>(q_hi - q_lo);
   // Work item w packs (head-in-group << 16 | query-tile index): no divisions on the roles'
   // per-tile path (a u32 div/mod is a ~100-cycle dependent chain).  n_work = end sentinel.
@@ -174,16 +147,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     mbar_init(kv_full, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&q_full[s], 1);
-      mbar_init(&q_empty[s], MC ? 2 : 1);  // MC: both CTAs' MMAs must have read the slot
+      mbar_init(&q_empty[s], 1);
     }
     mbar_init(do_full, 1);
-    mbar_init(do_empty, MC ? 2 : 1);
+    mbar_init(do_empty, 1);
     mbar_init(s_full, 1);
     mbar_init(p_full, NCOMP);
     mbar_init(dp_full, 1);
-    mbar_init(dp_full2[1], 1);
-    mbar_init(dq_full2[1], 1);
-    mbar_init(dq_free2[1], 128);
     mbar_init(ds_full, NCOMP);
     mbar_init(dq_full, 1);
     mbar_init(dq_free, 128);
@@ -198,13 +168,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   for (uint32_t b = threadIdx.x; b < (nr + 3) / 4; b += BWD_THREADS) {
     uint32_t byte = 0;
     for (uint32_t k = 0; k < 4; ++k)
-      if (4 * b + k < nr) {
-        const int64_t qt = q_lo + 4 * b + k;
-        int32_t cls = c0 < p.n_k ? bwd_class(p, qt, c0) : TILE_SKIP;
-        if (MC && cls == TILE_SKIP && c0p >= 0 && c0p < p.n_k && bwd_class(p, qt, c0p) != TILE_SKIP)
-          cls = TILE_PARTIAL;  // the partner needs this tile: compute it fully masked
-        byte |= static_cast<uint32_t>(cls) << (2 * k);
-      }
+      if (4 * b + k < nr) byte |= static_cast<uint32_t>(bwd_class(p, q_lo + 4 * b + k, c0)) << (2 * k);
     cls_tab[b] = static_cast<uint8_t>(byte);
   }
   auto tile_cls = [&](uint32_t qt) {
@@ -212,17 +176,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     return static_cast<int32_t>((cls_tab[x >> 2] >> ((x & 3) * 2)) & 3);
   };
   tc_fence_before();
-  if (MC)
-    cluster_sync();  // the partner's multicasts may target this CTA's barriers from here on
-  else
-    __syncthreads();
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   // Work items: (query head of the GQA group, query tile) in order, skipping masked tiles.
   // (nr == 0 must end at once: the class table is empty, and a head step must re-check the
-  // range -- reading an unwritten table entry once sent two CTAs of a multicast cluster down
-  // different item lists, a hang)
+  // range before reading a table entry)
   auto next_active = [&](int64_t w) {
     if (nr == 0) return n_work;
     for (;;) {
@@ -235,167 +195,152 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   auto item_qt = [&](int64_t w) { return static_cast<uint32_t>(q_lo) + static_cast<uint32_t>(w & 0xFFFF); };
   auto item_head = [&](int64_t w) { return kv_head * group + static_cast<int>(w >> 16); };
 
-  if (warp == 0) {
-    // ------------------------------------------------ TMA producer
-    if (elect_one()) {
-      mbar_expect_tx(kv_full, 2 * L::TILE);
-      for (int pn = 0; pn < PANELS; ++pn) {
-        tma_load_2d(smem + L::K_OFF + pn * 16384, &tk, kv_full, kv_head * D + pn * 64, static_cast<int32_t>(c0));
-        tma_load_2d(smem + L::V_OFF + pn * 16384, &tv, kv_full, kv_head * D + pn * 64, static_cast<int32_t>(c0));
-      }
-      uint32_t it = 0;
-      for (int64_t w = next_active(0); w < n_work; w = next_active(w + 1), ++it) {
-        const int32_t qrow0 = static_cast<int32_t>(item_qt(w) * 128);
-        const int h = item_head(w);
-        const uint32_t qs = it & 1;
-        BB_PROBE(0);
-        mbar_wait(&q_empty[qs], ((it >> 1) & 1) ^ 1);
-        BB_PROBE(1);
-        mbar_expect_tx(&q_full[qs], L::TILE);
+  if (warp < 4) {
+    setmaxnreg_dec<REGS_CTRL>();
+    if (warp == 0) {
+      // ------------------------------------------------ TMA producer
+      if (elect_one()) {
+        mbar_expect_tx(kv_full, 2 * L::TILE);
         for (int pn = 0; pn < PANELS; ++pn) {
-          if (!MC)
+          tma_load_2d(smem + L::K_OFF + pn * 16384, &tk, kv_full, kv_head * D + pn * 64, static_cast<int32_t>(c0));
+          tma_load_2d(smem + L::V_OFF + pn * 16384, &tv, kv_full, kv_head * D + pn * 64, static_cast<int32_t>(c0));
+        }
+        uint32_t it = 0;
+        for (int64_t w = next_active(0); w < n_work; w = next_active(w + 1), ++it) {
+          const int32_t qrow0 = static_cast<int32_t>(item_qt(w) * 128);
+          const int h = item_head(w);
+          const uint32_t qs = it & 1;
+          BB_PROBE(0);
+          mbar_wait(&q_empty[qs], ((it >> 1) & 1) ^ 1);
+          BB_PROBE(1);
+          mbar_expect_tx(&q_full[qs], L::TILE);
+          for (int pn = 0; pn < PANELS; ++pn)
             tma_load_2d(smem + L::Q_OFF + qs * L::TILE + pn * 16384, &tq, &q_full[qs], h * D + pn * 64, qrow0);
-          else if (crank == 0)
-            tma_load_2d_mc(smem + L::Q_OFF + qs * L::TILE + pn * 16384, &tq, &q_full[qs], h * D + pn * 64, qrow0, 3);
-        }
-        mbar_wait(do_empty, (it & 1) ^ 1);
-        BB_PROBE(2);
-        mbar_expect_tx(do_full, L::TILE);
-        for (int pn = 0; pn < PANELS; ++pn)
-          if (!MC)
+          mbar_wait(do_empty, (it & 1) ^ 1);
+          BB_PROBE(2);
+          mbar_expect_tx(do_full, L::TILE);
+          for (int pn = 0; pn < PANELS; ++pn)
             tma_load_2d(smem + L::DO_OFF + pn * 16384, &tdo, do_full, h * D + pn * 64, qrow0);
-          else if (crank == 0)
-            tma_load_2d_mc(smem + L::DO_OFF + pn * 16384, &tdo, do_full, h * D + pn * 64, qrow0, 3);
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
-    // Per tile t:  dV(t) [P(t) ready], S(t+1), dK(t) dQ(t) [dS(t) ready], dP(t+1) [dQ(t) drained].
-    // S(t+1) goes out as soon as dV(t) has been issued (the tensor pipe is in order, so dV(t)
-    // reads P(t) from the S columns before S(t+1) overwrites them); the compute warps then
-    // start P(t+1) while dK(t)/dQ(t) run and the drain warps empty dQ(t).
-    constexpr uint32_t idesc_st = idesc_bf16(128, 128, false, false);  // S^T, dP^T
-    constexpr uint32_t idesc_acc = idesc_bf16(128, D, false, true);    // dV (TS), dK: B MN-major
-    const uint32_t k_base = smem_u32(smem + L::K_OFF), v_base = smem_u32(smem + L::V_OFF);
-    const uint32_t do_base = smem_u32(smem + L::DO_OFF), ds_base = smem_u32(smem + L::DS_OFF);
-    auto issue_s = [&](uint32_t qs) {
-      const uint32_t q_base = smem_u32(smem + L::Q_OFF + qs * L::TILE);
-      if (elect_one()) {
-#pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
-          umma_ss(tmem + COL_S, sw128_desc(k_base + off, 16, 1024), sw128_desc(q_base + off, 16, 1024), idesc_st, ks > 0);
-        }
-        umma_commit(s_full);
-      }
-      __syncwarp();
-    };
-    constexpr uint32_t idesc_st64 = idesc_bf16(128, 64, false, false);  // dP^T half: 64 query columns
-    constexpr uint32_t idesc_dq64 = idesc_bf16(128, 64, true, true);    // dQ half: 64 head dims
-    constexpr uint32_t idesc_dq = idesc_bf16(128, D, true, true);       // dQ: A = dS (MN), B = K (MN)
-    auto issue_dp_half = [&](int g) {  // dP^T[:, 64g:64g+64] = V . dO[64g:64g+64]^T
-      if (elect_one()) {
-#pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
-          umma_ss(tmem + COL_DP + 64 * g, sw128_desc(v_base + off, 16, 1024),
-                  sw128_desc(do_base + off + 8192 * g, 16, 1024), idesc_st64, ks > 0);
-        }
-        umma_commit(dp_full2[g]);
-      }
-      __syncwarp();
-    };
-
-    mbar_wait(kv_full, 0);
-    int64_t w = next_active(0);
-    if (w < n_work) {
-      mbar_wait(&q_full[0], 0);
-      tc_fence_after();
-      issue_s(0);
-      mbar_wait(do_full, 0);
-      tc_fence_after();
-      issue_dp_half(0);
-      issue_dp_half(1);
-    }
-    for (uint32_t it = 0; w < n_work; ++it) {
-      const int64_t wn = next_active(w + 1);
-      const uint32_t qs = it & 1;
-      const uint32_t q_base = smem_u32(smem + L::Q_OFF + qs * L::TILE);
-      if (lane == 0) BB_PROBE(4);
-      mbar_wait(p_full, it & 1);
-      if (lane == 0) BB_PROBE(8);
-      tc_fence_after();
-      if (elect_one()) {
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {  // K = 128 query rows; P^T packed 2 per TMEM column
-          const uint32_t a_tmem = tmem + COL_S + (ks >> 1) * 32 + (ks & 1) * 8;  // P of q chunk c in its own S columns
-          umma_ts(tmem + COL_DV, a_tmem, sw128_desc(do_base + ks * 2048, 16384, 1024), idesc_acc, (it | ks) != 0);
-        }
-        if (MC)
-          umma_commit_mc(do_empty, 3);  // dP(t) and dV(t) have read dO(t) (both CTAs count)
-        else
-          umma_commit(do_empty);
-      }
-      __syncwarp();
-      if (wn < n_work) {
-        mbar_wait(&q_full[qs ^ 1], ((it + 1) >> 1) & 1);
-        tc_fence_after();
-        issue_s(qs ^ 1);
-      }
-      if (lane == 0) BB_PROBE(5);
-      mbar_wait(ds_full, it & 1);
-      if (lane == 0) BB_PROBE(9);
-      tc_fence_after();
-      if (elect_one()) {
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-          const uint64_t ad = sw128_desc(ds_base + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024);
-          umma_ss(tmem + COL_DK, ad, sw128_desc(q_base + ks * 2048, 16384, 1024), idesc_acc, (it | ks) != 0);
-        }
-        if (MC)
-          umma_commit_mc(&q_empty[qs], 3);
-        else
-          umma_commit(&q_empty[qs]);
-#if BB_BWD_DQ128
-        // one N=D MMA group (N=64 instructions are issue-bound at ~48 clk vs 32 nominal,
-        // tools/ubench_mma_rate.cu); both halves become ready together
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks)  // K = 128 keys
-          umma_ss(tmem + COL_DP, sw128_desc(ds_base + ks * 2048, 16384, 1024),
-                  sw128_desc(k_base + ks * 2048, 16384, 1024), idesc_dq, ks > 0);
-#pragma unroll
-        for (int h = 0; h < D / 64; ++h) umma_commit(dq_full2[h]);
-#else
-#pragma unroll
-        for (int h = 0; h < D / 64; ++h) {
-#pragma unroll
-          for (int ks = 0; ks < 8; ++ks)  // K = 128 keys; N = head dims [64h, 64h+64)
-            umma_ss(tmem + COL_DP + 64 * h, sw128_desc(ds_base + ks * 2048, 16384, 1024),
-                    sw128_desc(k_base + ks * 2048 + 16384 * h, 16384, 1024), idesc_dq64, ks > 0);
-          umma_commit(dq_full2[h]);
-        }
-#endif
-      }
-      __syncwarp();
-      if (wn < n_work) {
-        mbar_wait(do_full, (it + 1) & 1);
-        if (lane == 0) BB_PROBE(6);
-#pragma unroll
-        for (int g = 0; g < 2; ++g) {
-          if (64 * g < D) {  // these dP^T columns held dQ half g of tile t
-            mbar_wait(dq_free2[g], it & 1);
-            tc_fence_after();
+          // dO is single-buffered: dO(t+1) can only be loaded once dV(t) has read dO(t), which
+          // puts its HBM latency (~2k cycles under load) between dV(t) and dP(t+1).  Warm L2
+          // with the next item's dO and Q now, a whole tile ahead, so that load hits L2.
+          const int64_t wn = next_active(w + 1);
+          if (wn < n_work) {
+            const int32_t nrow0 = static_cast<int32_t>(item_qt(wn) * 128);
+            const int nh = item_head(wn);
+            for (int pn = 0; pn < PANELS; ++pn) {
+              tma_prefetch_l2_2d(&tdo, nh * D + pn * 64, nrow0);
+              tma_prefetch_l2_2d(&tq, nh * D + pn * 64, nrow0);
+            }
           }
-          if (lane == 0 && g == 0) BB_PROBE(7);
-          issue_dp_half(g);
         }
       }
-      w = wn;
+    } else if (warp == 1) {
+      // ------------------------------------------------ MMA issuer
+      // Per tile t:  dV(t) [P(t) ready], S(t+1), dK(t) dQ(t) [dS(t) ready], dP(t+1) [dQ(t) read].
+      // S(t+1) goes out as soon as dV(t) has been issued (the tensor pipe is in order, so dV(t)
+      // reads P(t) from the S columns before S(t+1) overwrites them); the compute warps then
+      // start P(t+1) while dK(t)/dQ(t) run, and dP(t+1) follows dQ(t) as soon as the drain has
+      // pulled dQ(t) into registers, as one N=128 group.
+      constexpr uint32_t idesc_st = idesc_bf16(128, 128, false, false);  // S^T, dP^T
+      constexpr uint32_t idesc_acc = idesc_bf16(128, D, false, true);    // dV (TS), dK: B MN-major
+      constexpr uint32_t idesc_dq = idesc_bf16(128, D, true, true);      // dQ: A = dS (MN), B = K (MN)
+      const uint32_t k_base = smem_u32(smem + L::K_OFF), v_base = smem_u32(smem + L::V_OFF);
+      const uint32_t do_base = smem_u32(smem + L::DO_OFF), ds_base = smem_u32(smem + L::DS_OFF);
+      auto issue_s = [&](uint32_t qs) {
+        const uint32_t q_base = smem_u32(smem + L::Q_OFF + qs * L::TILE);
+        if (elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < D / 16; ++ks) {
+            const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
+            umma_ss(tmem + COL_S, sw128_desc(k_base + off, 16, 1024), sw128_desc(q_base + off, 16, 1024), idesc_st,
+                    ks > 0);
+          }
+          umma_commit(s_full);
+        }
+        __syncwarp();
+      };
+      auto issue_dp = [&]() {  // dP^T = V . dO^T
+        if (elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < D / 16; ++ks) {
+            const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
+            umma_ss(tmem + COL_DP, sw128_desc(v_base + off, 16, 1024), sw128_desc(do_base + off, 16, 1024), idesc_st,
+                    ks > 0);
+          }
+          umma_commit(dp_full);
+        }
+        __syncwarp();
+      };
+
+      mbar_wait(kv_full, 0);
+      int64_t w = next_active(0);
+      if (w < n_work) {
+        mbar_wait(&q_full[0], 0);
+        tc_fence_after();
+        issue_s(0);
+        mbar_wait(do_full, 0);
+        tc_fence_after();
+        issue_dp();
+      }
+      for (uint32_t it = 0; w < n_work; ++it) {
+        const int64_t wn = next_active(w + 1);
+        const uint32_t qs = it & 1;
+        const uint32_t q_base = smem_u32(smem + L::Q_OFF + qs * L::TILE);
+        if (lane == 0) BB_PROBE(4);
+        mbar_wait(p_full, it & 1);
+        if (lane == 0) BB_PROBE(8);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {  // K = 128 query rows; P^T packed 2 per TMEM column
+            const uint32_t a_tmem = tmem + COL_S + (ks >> 1) * 32 + (ks & 1) * 8;  // P of q chunk c in its own S columns
+            umma_ts(tmem + COL_DV, a_tmem, sw128_desc(do_base + ks * 2048, 16384, 1024), idesc_acc, (it | ks) != 0);
+          }
+          umma_commit(do_empty);
+        }
+        __syncwarp();
+        if (wn < n_work) {
+          mbar_wait(&q_full[qs ^ 1], ((it + 1) >> 1) & 1);
+          tc_fence_after();
+          issue_s(qs ^ 1);
+        }
+        if (lane == 0) BB_PROBE(5);
+        mbar_wait(ds_full, it & 1);
+        if (lane == 0) BB_PROBE(9);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {  // dS^T of q chunk c packed over its own dP^T columns (TS)
+            const uint32_t a_tmem = tmem + COL_DP + (ks >> 1) * 32 + (ks & 1) * 8;
+            umma_ts(tmem + COL_DK, a_tmem, sw128_desc(q_base + ks * 2048, 16384, 1024), idesc_acc, (it | ks) != 0);
+          }
+          umma_commit(&q_empty[qs]);
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)  // K = 128 keys
+            umma_ss(tmem + COL_DP, sw128_desc(ds_base + ks * 2048, 16384, 1024),
+                    sw128_desc(k_base + ks * 2048, 16384, 1024), idesc_dq, ks > 0);
+          umma_commit(dq_full);
+        }
+        __syncwarp();
+        if (lane == 0) BB_PROBE(10);
+        if (wn < n_work) {
+          mbar_wait(do_full, (it + 1) & 1);
+          if (lane == 0) BB_PROBE(6);
+          mbar_wait(dq_free, it & 1);  // these dP^T columns held dQ(t)
+          if (lane == 0) BB_PROBE(7);
+          tc_fence_after();
+          issue_dp();
+          if (lane == 0) BB_PROBE(11);
+        }
+        w = wn;
+      }
+      if (elect_one()) umma_commit(acc_full);
+      __syncwarp();
     }
-    if (elect_one()) umma_commit(acc_full);
-    __syncwarp();
-  } else if (warp >= 4 && warp < 4 + 4 * NG) {
+  } else if (warp < 4 + 4 * NG) {
     // ------------------------------------------------ P / dS (two column groups) + epilogue
+    setmaxnreg_inc<REGS_COMP>();
     const int g = (warp - 4) >> 2;             // column group: query columns [CPG*g, CPG*(g+1))
     const uint32_t quad = warp & 3;
     const int row = quad * 32 + lane;          // key row of S^T / dP^T
@@ -407,52 +352,70 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     const int64_t k_id = key_ok ? token_id(p.layout, p.k_device, krow) : 0;
     uint8_t* ds_tile = smem + L::DS_OFF;
 
-    // Raw global value only: the transform is applied at the smem store so the load's
-    // latency hides under the tile instead of stalling the loop top.
-    auto load_vec = [&](int64_t w) {  // threads 0..127: lse of query ct; 128..255: delta
-      const int64_t r = item_qt(w) * 128 + (ct & 127);
-      if (r >= p.n_q) return ct < 128 ? -INFINITY : 0.f;
-      const int64_t at = static_cast<int64_t>(item_head(w)) * p.n_q + r;
-      return __ldg((ct < 128 ? p.lse : p.delta) + at);
+    // lse / D of the group's 64 query columns live in a per-group smem copy, so only the 128
+    // threads of a group synchronise on it (named barrier 5 + g), never the two groups with
+    // each other.  Thread gt of the group fetches one value for the next item during the dS
+    // pass (gt < 64: lse of column 64g + gt; else D of column 64g + gt - 64); the transform is
+    // applied at the store so the load's latency hides there.
+    const int gt = ct & 127;
+    float* vec_g = reinterpret_cast<float*>(smem + L::VEC_OFF + g * 512);  // [lse2 64 | -D 64]
+    const float* lse2 = vec_g - CPG * g;  // indexed by the tile's query column (group g: [64g, 64g+64))
+    const float* dlt = vec_g + 64 - CPG * g;
+    auto load_vec = [&](int64_t w) {
+      const int64_t r = static_cast<int64_t>(item_qt(w)) * 128 + CPG * g + (gt & 63);
+      if (r >= p.n_q) return gt < 64 ? -INFINITY : 0.f;
+      return __ldg((gt < 64 ? p.lse : p.delta) + static_cast<int64_t>(item_head(w)) * p.n_q + r);
     };
-    auto vec_val = [&](float raw) {  // stored negated for the packed FFMA2 / FADD2 forms:
-      if (ct >= 128) return -raw;       //   -D,  and -lse*log2e (-inf row -> -inf, so P = 0)
-      return raw == -INFINITY ? -INFINITY : -raw * 1.4426950408889634f;
+    auto store_vec = [&](float raw) {  // stored negated for the packed FFMA2 / FADD2 forms:
+      vec_g[gt] = gt >= 64 ? -raw : raw == -INFINITY ? -INFINITY : -raw * 1.4426950408889634f;  // -D, -lse*log2e
     };
+    auto group_sync = [&]() { named_bar_sync(5 + g, 128); };
 
+    // The next item, its class and its lse / D are looked up while this tile's dP^T is still
+    // in flight (between the P and dS passes), so the loop top is just the S^T wait: the
+    // class-table walk is a chain of dependent shared loads.
     int64_t w = next_active(0);
-    if (w < n_work && ct < 256) vec_s[ct] = vec_val(load_vec(w));
-    named_bar_sync(3, NCOMP);
+    int32_t cls = w < n_work ? tile_cls(item_qt(w)) : TILE_SKIP;
+    if (w < n_work) store_vec(load_vec(w));
     uint32_t it = 0;
     while (w < n_work) {
       if (ct == 0) BB_PROBE(24);
-      const int32_t cls = tile_cls(item_qt(w));
-      const int64_t r0 = static_cast<int64_t>(item_qt(w)) * 128;
-      const int64_t w_next = next_active(w + 1);
-      const float v_next = (w_next < n_work && ct < 256) ? load_vec(w_next) : 0.f;  // prefetch under this tile
-      const float* lse2 = vec_s;
-      const float* dlt = lse2 + 128;
+      if (ct == 128) BB_PROBE(25);
       uint4 bits = make_uint4(~0u, ~0u, ~0u, ~0u);
-      if (cls == TILE_PARTIAL) bits = row_mask_bits(p.layout, p.mask, k_id, key_ok, p.q_device, r0, p.n_q, false);
-      else if (!key_ok) bits = make_uint4(0u, 0u, 0u, 0u);
+      if (cls == TILE_PARTIAL)
+        bits = row_mask_bits(p.layout, p.mask, k_id, key_ok, p.q_device, static_cast<int64_t>(item_qt(w)) * 128,
+                             p.n_q, false);
+      else if (!key_ok)
+        bits = make_uint4(0u, 0u, 0u, 0u);
       if (ct == 0) BB_PROBE(16);
       mbar_wait(s_full, it & 1);
       if (ct == 0) BB_PROBE(17);
+      if (ct == 128) BB_PROBE(26);
       tc_fence_after();
+      group_sync();  // this tile's lse / D (stored at the end of the last one) are visible
 
       // ---- P^T = exp2(S^T * scale*log2e - lse2[q]) -> TMEM (bf16 pairs, over S^T); kept packed.
       // lse2 of a 32-query chunk is read from smem before the TMEM load so the LDS latency
       // hides under it (tcgen05.wait::ld is a compiler memory barrier).  Only partial tiles
       // (and a ragged last key tile) pay for the per-element mask.
+      // Every shared-memory load this tile needs is issued well ahead of its first use: under the
+      // SS MMAs' operand fetch (128 B/clk, the whole port) an LDS waits hundreds of cycles, and
+      // the warp issues in order.  lse of both chunks now; the class byte of the next query
+      // tile now (read after the P pass); -D of both chunks right after the P pass.
+      float l2[CH][32];
+#pragma unroll
+      for (int c2 = 0; c2 < CH; ++c2)
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(&l2[c2][i]) = *reinterpret_cast<const float4*>(&lse2[(g * CH + c2) * 32 + i]);
+      const uint32_t nxt = item_qt(w) + 1 - static_cast<uint32_t>(q_lo);  // next tile's class-table index
+      const uint32_t cls_byte = nxt < nr ? cls_tab[nxt >> 2] : 0u;
       uint32_t pk[CH][16];
       auto p_pass = [&](auto masked_tag) {
         constexpr bool MASKED = decltype(masked_tag)::value;
 #pragma unroll
         for (int c2 = 0; c2 < CH; ++c2) {
           const int c = g * CH + c2;
-          float l2[32];
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(&l2[i]) = *reinterpret_cast<const float4*>(&lse2[c * 32 + i]);
           float s[32];
           tmem_ld32(tmem + t_lane + COL_S + c * 32, s);
           tmem_ld_wait();
@@ -460,7 +423,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           for (int i = 0; i < 32; i += 2) {
             const int qc = c * 32 + i;
             const float2 x = __ffma2_rn(make_float2(s[i], s[i + 1]), make_float2(p.scale_log2, p.scale_log2),
-                                        make_float2(l2[i], l2[i + 1]));  // l2 = -lse*log2e
+                                        make_float2(l2[c2][i], l2[c2][i + 1]));  // l2 = -lse*log2e
             float e0 = ex2_approx(x.x);
             float e1 = ex2_approx(x.y);
             if (MASKED) {
@@ -480,30 +443,50 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       tc_fence_before();
       mbar_arrive(p_full);
       if (ct == 0) BB_PROBE(18);
+      if (ct == 128) BB_PROBE(27);
+      float dl[CH][32];
+#pragma unroll
+      for (int c2 = 0; c2 < CH; ++c2)
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(&dl[c2][i]) = *reinterpret_cast<const float4*>(&dlt[(g * CH + c2) * 32 + i]);
+      // Next item: the following query tile of the same head unless the prefetched class says
+      // it is masked out (or the range ends); the general walk only then.
+      int64_t w_next;
+      int32_t cls_next;
+      const int32_t c_adj = static_cast<int32_t>((cls_byte >> ((nxt & 3) * 2)) & 3);
+      if (nxt < nr && c_adj != TILE_SKIP) {
+        w_next = w + 1;
+        cls_next = c_adj;
+      } else {
+        w_next = next_active(w + 1);
+        cls_next = w_next < n_work ? tile_cls(item_qt(w_next)) : TILE_SKIP;
+      }
+      const float v_next = w_next < n_work ? load_vec(w_next) : 0.f;  // lands during the dS pass
 
       // ---- dS^T = P^T o (dP^T - D[q]) -> smem (K-major rows = keys); the dK/dQ MMAs of the
-      // previous tile must have finished reading the buffer: dP_g(t) is issued after dK(t-1)
+      // previous tile must have finished reading the buffer: dP(t) is issued after dK(t-1)
       // and dQ(t-1), so its commit covers them.
-      mbar_wait(dp_full2[NG == 2 ? g : 1], it & 1);
-      if (NG != 2) mbar_wait(dp_full2[0], it & 1);
+      if (ct == 0) BB_PROBE(30);
+      if (ct == 128) BB_PROBE(31);
+      mbar_wait(dp_full, it & 1);
       if (ct == 0) BB_PROBE(19);
+      if (ct == 128) BB_PROBE(28);
       tc_fence_after();
 #pragma unroll
       for (int c2 = 0; c2 < CH; ++c2) {
         const int c = g * CH + c2;
-        float dl[32];
-#pragma unroll
-        for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(&dl[i]) = *reinterpret_cast<const float4*>(&dlt[c * 32 + i]);
         float dp[32];
         tmem_ld32(tmem + t_lane + COL_DP + c * 32, dp);
         tmem_ld_wait();
 #pragma unroll
         for (int a = 0; a < 32; a += 2) {  // dS^T packed in place of P^T
           const __nv_bfloat162 pb = *reinterpret_cast<const __nv_bfloat162*>(&pk[c2][a / 2]);
-          const float2 ds = __fmul2_rn(__fadd2_rn(make_float2(dp[a], dp[a + 1]), make_float2(dl[a], dl[a + 1])),
+          const float2 ds = __fmul2_rn(__fadd2_rn(make_float2(dp[a], dp[a + 1]), make_float2(dl[c2][a], dl[c2][a + 1])),
                                        make_float2(__low2float(pb), __high2float(pb)));  // dl = -D
           pk[c2][a / 2] = pack_bf16(ds.x, ds.y);
         }
+        tmem_st16(tmem + t_lane + COL_DP + c * 32, pk[c2]);  // dK's A operand (TS)
       }
 #pragma unroll
       for (int c2 = 0; c2 < CH; ++c2)
@@ -512,15 +495,17 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           *reinterpret_cast<uint4*>(ds_tile + sw128_offset(row, (g * CH + c2) * 32 + i, 16384)) =
               make_uint4(pk[c2][i / 2], pk[c2][i / 2 + 1], pk[c2][i / 2 + 2], pk[c2][i / 2 + 3]);
       fence_async_smem();
+      tmem_st_wait();
       tc_fence_before();
       mbar_arrive(ds_full);
       if (ct == 0) BB_PROBE(20);
+      if (ct == 128) BB_PROBE(29);
 
-      named_bar_sync(3, NCOMP);  // everyone is done with this tile's lse / D
-      if (w_next < n_work && ct < 256) vec_s[ct] = vec_val(v_next);
-      named_bar_sync(3, NCOMP);
+      group_sync();  // the group is done with this tile's lse / D
+      if (w_next < n_work) store_vec(v_next);
       if (ct == 0) BB_PROBE(23);
       w = w_next;
+      cls = cls_next;
       ++it;
     }
     // ---- dK (scaled) and dV accumulate into the resident fp32 buffers
@@ -556,49 +541,53 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         }
       }
     }
-  } else if (warp >= 4 + 4 * NG) {
+  } else {
     // ------------------------------------------------ dQ drain (TMEM lane = query row)
-    // dQ(t) -> swizzled smem staging (two 32-column chunks at a time) -> TMA bulk reduce-add
-    // (fp32) into the circulating dQ; each TMEM half is released (dq_free) as soon as it has
-    // been read.
+    // The whole dQ(t) row comes out of TMEM at once (D fp32 registers per thread) and its
+    // columns are released (dq_free) before any staging, so dP(t+1) never waits on the
+    // reduce; then D/32 chunks of 32 columns alternate between the two 16 KB staging slots,
+    // each a TMA bulk reduce-add (fp32) into the circulating dQ.  A slot is restaged once the
+    // reduce issued from it two chunks earlier has finished reading it (bulk_wait_read<1>).
+    setmaxnreg_inc<REGS_DRAIN>();
+    constexpr int CHUNKS = D / 32;
+    // (16-column chunks through 8 KB SWIZZLE_64B slots measured 10 % slower: twice the
+    // barriers per tile, and half-line reduce rows.
+    // red.global.add.v4.f32 from registers for half the columns measured 20 % slower overall:
+    // the one-row-per-lane pattern floods the LSU / MIO queue the compute warps' tcgen05.ld/st
+    // go through, doubling their P pass.)
     const uint32_t quad = warp & 3;
     const int row = quad * 32 + lane;
     const uint32_t t_lane = (quad * 32) << 16;
     const bool issuer = (quad == 0 && lane == 0);
     uint8_t* stg = smem + L::STG_OFF;
-    constexpr int CHUNKS = D / 32;
-    auto stage = [&](const float (&v)[32], int slot) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float4 x = make_float4(v[4 * i] * p.scale, v[4 * i + 1] * p.scale, v[4 * i + 2] * p.scale,
-                                     v[4 * i + 3] * p.scale);
-        *reinterpret_cast<float4*>(stg + slot * 16384 + row * 128 + ((i ^ (row & 7)) << 4)) = x;
-      }
-    };
-    uint32_t it = 0;
+    uint32_t it = 0, chunk = 0;
     for (int64_t w = next_active(0); w < n_work; w = next_active(w + 1), ++it) {
       const int32_t qrow0 = static_cast<int32_t>(item_qt(w) * 128);
       const int hcol = item_head(w) * D;
       if (row == 0) BB_PROBE(21);
+      mbar_wait(dq_full, it & 1);
+      tc_fence_after();
+      float v[CHUNKS][32];
 #pragma unroll
-      for (int half = 0; half < CHUNKS / 2; ++half) {
-        mbar_wait(dq_full2[half], it & 1);
-        tc_fence_after();
-        float a[32], b[32];
-        tmem_ld32(tmem + t_lane + COL_DP + half * 64, a);
-        tmem_ld32(tmem + t_lane + COL_DP + half * 64 + 32, b);
-        tmem_ld_wait();
-        tc_fence_before();  // this half of dQ(t) is read: release its TMEM columns
-        mbar_arrive(dq_free2[half]);
-        if (issuer) bulk_wait_read<0>();  // previous reduce finished reading the staging
+      for (int c = 0; c < CHUNKS; ++c) tmem_ld32(tmem + t_lane + COL_DP + c * 32, v[c]);
+      tmem_ld_wait();
+      tc_fence_before();  // dQ(t) is in registers: its TMEM columns go back to dP(t+1)
+      mbar_arrive(dq_free);
+#pragma unroll
+      for (int c = 0; c < CHUNKS; ++c, ++chunk) {
+        const uint32_t slot = chunk & 1;
+        if (issuer) bulk_wait_read<1>();  // the reduce issued from this slot has read it
         named_bar_sync(4, 128);
-        stage(a, 0);
-        stage(b, 1);
+        uint8_t* dst = stg + slot * 16384 + row * 128;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          *reinterpret_cast<float4*>(dst + ((i ^ (row & 7)) << 4)) =
+              make_float4(v[c][4 * i] * p.scale, v[c][4 * i + 1] * p.scale, v[c][4 * i + 2] * p.scale,
+                          v[c][4 * i + 3] * p.scale);
         fence_async_smem();
         named_bar_sync(4, 128);
         if (issuer) {
-          tma_reduce_add_2d(&tdq, stg, hcol + half * 64, qrow0);
-          tma_reduce_add_2d(&tdq, stg + 16384, hcol + half * 64 + 32, qrow0);
+          tma_reduce_add_2d(&tdq, stg + slot * 16384, hcol + c * 32, qrow0);
           bulk_commit();
         }
       }
@@ -608,10 +597,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   }
 
   tc_fence_before();
-  if (MC)
-    cluster_sync();  // no CTA leaves while its partner may still multicast into it
-  else
-    __syncthreads();
+  __syncthreads();
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
@@ -657,25 +643,8 @@ int launch_bwd_d(const bb_attn_bwd_args& a, cudaStream_t st) {
     attr_done |= uint64_t(1) << dev;
   }
   const unsigned n_kt = static_cast<unsigned>((a.n_k + 127) / 128);
-  if (MC) {  // clusters of two adjacent key tiles (an odd count gets an empty partner)
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((n_kt + 1) & ~1u, n_heads);
-    cfg.blockDim = dim3(BWD_THREADS);
-    cfg.dynamicSmemBytes = BwdSmem<D>::BYTES;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (check_cuda(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tdo, tdq, p), "attn_bwd cluster launch"))
-      return BB_ERR_CUDA;
-  } else {
-    dim3 grid(n_kt, n_heads);
-    kern<<<grid, BWD_THREADS, BwdSmem<D>::BYTES, st>>>(tq, tk, tv, tdo, tdq, p);
-  }
+  dim3 grid(n_kt, n_heads);
+  kern<<<grid, BWD_THREADS, BwdSmem<D>::BYTES, st>>>(tq, tk, tv, tdo, tdq, p);
   return check_launch("attn_bwd_kernel");
 }
 

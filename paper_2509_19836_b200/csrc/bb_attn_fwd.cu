@@ -289,7 +289,7 @@ __device__ __forceinline__ void fwd_softmax_split(const FwdParams& p, uint8_t* x
 template <int D, bool SPLIT>
 __global__ void __launch_bounds__(fwd_threads<SPLIT>(), 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
-                    const __grid_constant__ CUtensorMap tv, const FwdParams p) {
+                    const __grid_constant__ CUtensorMap tv, const __grid_constant__ FwdParams p) {
   using L = FwdSmem<D, SPLIT>;
   constexpr int PANELS = D / 64;
   constexpr int KV_SLOTS = kv_slots<SPLIT>();

@@ -8,14 +8,12 @@
 //   exp_shifted_f64   numerics.py:101-107 exp(s - lse[:, None]); lse == -inf rows give 0
 //   exp_gap_f64       numerics.py:110-116 exp(a - b); a == -inf gives 0
 //   rowsum_hadamard   numerics.py:86-92   out[i] = sum_j a[i,j] b[i,j]
-//   scale_mask_f64    oracle.py:66-75     masked_scores: S * scale, masked entries -inf
+//   scale_mask_f64    oracle.py:66-75     masked_scores: S / sqrt(d), masked entries -inf
 //   xent_f64          oracle.py:129-154   loss = lse - logit[y], g = softmax - onehot(y)
 // All are HBM-bound (one read of each operand, one write) except matmul, which runs on the
 // FP64 pipe with a 64x64 CTA tile staged in shared memory.
 #include <cuda_runtime.h>
 #include <math_constants.h>
-
-#include <algorithm>
 
 #include <algorithm>
 
@@ -123,12 +121,13 @@ __global__ void xent_kernel(const double* __restrict__ logits, const double* __r
   if (lane == 0) loss[r] = -row[y] + l;
 }
 
-// s[i] = allowed[i] ? s[i] * scale : -inf, in place (oracle.py:73-75 after the Q K^T product).
-__global__ void scale_mask_kernel(double* __restrict__ s, const uint8_t* __restrict__ allowed, double scale,
+// s[i] = allowed[i] ? s[i] / root : -inf, in place (oracle.py:73-75 after the Q K^T product;
+// a division like the reference's `/ np.sqrt(d)`, not a multiply by its reciprocal).
+__global__ void scale_mask_kernel(double* __restrict__ s, const uint8_t* __restrict__ allowed, double root,
                                   int64_t n) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    s[i] = allowed[i] ? s[i] * scale : -CUDART_INF;
+    s[i] = allowed[i] ? s[i] / root : -CUDART_INF;
 }
 
 // C[m, n] = sum_k A[m, k] B[k, n] in float64, k ascending for every element.

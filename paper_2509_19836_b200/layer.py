@@ -27,7 +27,7 @@ import torch
 from . import _native as N
 from . import kernels as K
 from .distributed import AttentionGrads, AttentionResult
-from .masks import BLOCK_SPARSE, MaskSpec, validate_mask
+from .masks import BLOCK_SPARSE, SLIDING_WINDOW, MaskSpec, validate_mask
 from .partitioning import ShardLayout, device_token_ids
 
 
@@ -153,7 +153,12 @@ def project_qkv_shards(x, params: AttentionParams, layout: ShardLayout, heads: i
 
 
 def _first_empty_row(mask: MaskSpec, nq: int, nk: int) -> int | None:
-    """0-based first query row with no allowed key (only block-sparse masks can have one)."""
+    """0-based first query row with no allowed key among keys 1..nk (oracle.py:88-91 raises
+    for it).  Full and causal masks always leave key 1; a sliding window empties rows
+    q >= nk + w; a block-sparse mask empties rows whose block row has no block before nk."""
+    if mask.kind == SLIDING_WINDOW:
+        r = nk + int(mask.window) - 1  # first id q = r + 1 with q - nk >= w
+        return r if r < nq else None
     if mask.kind != BLOCK_SPARSE:
         return None
     bm = np.asarray(mask.block_mask) != 0
@@ -180,9 +185,16 @@ def masked_scores(q, k, mask: MaskSpec, device=None):
     validate_mask(mask, max(qt.shape[0], kt.shape[0]))
     s = F.matmul(qt, kt.t())
     allowed = torch.from_numpy(np.ascontiguousarray(dense_mask(mask, qt.shape[0], kt.shape[0]), dtype=np.uint8)).to(dev)
-    N.check(N.load().bb_scale_mask_f64(s.data_ptr(), allowed.data_ptr(), 1.0 / math.sqrt(qt.shape[1]), s.numel(),
-                                       C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+    with torch.cuda.device(dev):
+        N.check(N.load().bb_scale_mask_f64(s.data_ptr(), allowed.data_ptr(), math.sqrt(qt.shape[1]), s.numel(),
+                                           C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
     return s.cpu().numpy() if host else s
+
+
+def _single_device_layout(nq: int, nk: int) -> ShardLayout:
+    """One shard holding ids 1..max(nq, nk): queries are its first nq rows, keys its first nk
+    (dense_mask's id convention, masks.py:89-104); rows past either count are never read."""
+    return ShardLayout("contiguous", max(nq, nk), 1)
 
 
 def attention_forward(q, k, v, mask: MaskSpec, device=None) -> AttentionResult:
@@ -194,8 +206,6 @@ def attention_forward(q, k, v, mask: MaskSpec, device=None) -> AttentionResult:
         raise ValueError("Q, K, V must share the model dimension")
     nq, nk, d = q.shape[0], k.shape[0], q.shape[1]
     validate_mask(mask, max(nq, nk))
-    if nq > nk:
-        raise ValueError(f"{nq} query rows > {nk} keys: the ring kernels take at most one query per key row")
     bad = _first_empty_row(mask, nq, nk)
     if bad is not None:
         raise ValueError(f"query row {bad + 1} has no unmasked key")
@@ -203,11 +213,12 @@ def attention_forward(q, k, v, mask: MaskSpec, device=None) -> AttentionResult:
     dp = 64 if d <= 64 else 128
     if d > 128:
         raise ValueError(f"model dimension {d} > 128: split it into heads (the kernels take d <= 128)")
-    qb, kb, vb = (_bf16_padded(t, dev, dp).view(-1, 1, dp) for t in (q, k, v))
-    layout = ShardLayout("contiguous", nk, 1)
-    o = torch.zeros(nq, 1, dp, device=dev)
-    lse = torch.full((1, nq), float("-inf"), device=dev)
-    K.attn_fwd_step(qb, kb, vb, o, lse, layout, K.device_mask(mask, dev), 1, 1, 1.0 / math.sqrt(d), n_q=nq)
+    with torch.cuda.device(dev):
+        qb, kb, vb = (_bf16_padded(t, dev, dp).view(-1, 1, dp) for t in (q, k, v))
+        o = torch.zeros(nq, 1, dp, device=dev)
+        lse = torch.full((1, nq), float("-inf"), device=dev)
+        K.attn_fwd_step(qb, kb, vb, o, lse, _single_device_layout(nq, nk), K.device_mask(mask, dev), 1, 1,
+                        1.0 / math.sqrt(d), n_q=nq)
     res = AttentionResult(o=o[:, 0, :d], lse=lse[0])
     if isinstance(q, torch.Tensor):
         return res
@@ -215,30 +226,44 @@ def attention_forward(q, k, v, mask: MaskSpec, device=None) -> AttentionResult:
 
 
 def attention_backward(q, k, v, o, lse, do, mask: MaskSpec, device=None) -> AttentionGrads:
-    """Gradients of sum(O * dO) w.r.t. Q, K, V (oracle.py:98-119), one device."""
+    """Gradients of sum(O * dO) w.r.t. Q, K, V (oracle.py:98-119), one device.
+
+    Checks what the reference's masked_scores / matmul chain rejects (oracle.py:66-75,
+    108-119) before any device memory is touched: Q/K model dims, K/V rows, dO and O shapes,
+    the mask against max(nq, nk), and the lse length."""
     q, k, v, do = _matrix(q, "Q"), _matrix(k, "K"), _matrix(v, "V"), _matrix(do, "dO")
     o = _matrix(o, "O")
     if tuple(do.shape) != (q.shape[0], v.shape[1]):
         raise ValueError(f"dO must be {q.shape[0]}x{v.shape[1]}, got {tuple(do.shape)}")
+    if q.shape[1] != k.shape[1]:
+        raise ValueError(f"Q has dim {q.shape[1]} but K has dim {k.shape[1]}")
+    if k.shape[0] != v.shape[0]:
+        raise ValueError(f"K has {k.shape[0]} rows but V has {v.shape[0]}")
+    if v.shape[1] != q.shape[1]:
+        raise ValueError("Q, K, V must share the model dimension")
+    if tuple(o.shape) != tuple(do.shape):
+        raise ValueError(f"O must be {do.shape[0]}x{do.shape[1]}, got {tuple(o.shape)}")
     nq, nk, d = q.shape[0], k.shape[0], q.shape[1]
-    if nq > nk:
-        raise ValueError(f"{nq} query rows > {nk} keys: the ring kernels take at most one query per key row")
+    validate_mask(mask, max(nq, nk))
+    lt = lse if isinstance(lse, torch.Tensor) else torch.from_numpy(np.asarray(lse, dtype=np.float64))
+    if lt.numel() != nq:
+        raise ValueError(f"lse must have {nq} entries, got {lt.numel()}")
     if d > 128:
         raise ValueError(f"model dimension {d} > 128: split it into heads (the kernels take d <= 128)")
     dev = _device(device)
     dp = 64 if d <= 64 else 128
-    qb, kb, vb, dob = (_bf16_padded(t, dev, dp).view(-1, 1, dp) for t in (q, k, v, do))
-    ot = o if isinstance(o, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(o))
-    ot = torch.nn.functional.pad(ot.to(device=dev, dtype=torch.float32), (0, dp - d)).view(-1, 1, dp).contiguous()
-    lt = lse if isinstance(lse, torch.Tensor) else torch.from_numpy(np.asarray(lse, dtype=np.float64))
-    lt = lt.to(device=dev, dtype=torch.float32).reshape(1, nq).contiguous()
-    layout = ShardLayout("contiguous", nk, 1)
-    delta = torch.empty(1, nq, device=dev)
-    K.bwd_preprocess(dob, ot, delta)
-    dq = torch.zeros(nq, 1, dp, device=dev)
-    dk = torch.zeros(nk, 1, dp, device=dev)
-    dv = torch.zeros(nk, 1, dp, device=dev)
-    K.attn_bwd_step(qb, kb, vb, dob, lt, delta, dq, dk, dv, layout, K.device_mask(mask, dev), 1, 1, 1.0 / math.sqrt(d))
+    with torch.cuda.device(dev):
+        qb, kb, vb, dob = (_bf16_padded(t, dev, dp).view(-1, 1, dp) for t in (q, k, v, do))
+        ot = o if isinstance(o, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(o))
+        ot = torch.nn.functional.pad(ot.to(device=dev, dtype=torch.float32), (0, dp - d)).view(-1, 1, dp).contiguous()
+        lt = lt.to(device=dev, dtype=torch.float32).reshape(1, nq).contiguous()
+        delta = torch.empty(1, nq, device=dev)
+        K.bwd_preprocess(dob, ot, delta)
+        dq = torch.zeros(nq, 1, dp, device=dev)
+        dk = torch.zeros(nk, 1, dp, device=dev)
+        dv = torch.zeros(nk, 1, dp, device=dev)
+        K.attn_bwd_step(qb, kb, vb, dob, lt, delta, dq, dk, dv, _single_device_layout(nq, nk), K.device_mask(mask, dev),
+                        1, 1, 1.0 / math.sqrt(d))
     grads = AttentionGrads(dq=dq[:, 0, :d], dk=dk[:, 0, :d], dv=dv[:, 0, :d])
     if isinstance(q, torch.Tensor):
         return grads

@@ -51,7 +51,14 @@ def _bad_fwd_args(**over):
         ({"hq": 3}, "multiple of hkv"),
         ({"head_dim": 96}, "head_dim"),
         ({"q_device": 2}, "device indices"),
-        ({"n_k": 4}, "shard sizes"),
+        ({"n_k": 16}, "shard sizes"),
+        ({"n_q": 9}, "shard sizes"),
+        ({"layout": N.BbLayout(kind=1, devices=3, seq_len=9, block_len=0)}, "zigzag"),
+        ({"layout": N.BbLayout(kind=0, devices=3, seq_len=8, block_len=0)}, "divisible by 3 devices"),
+        ({"layout": N.BbLayout(kind=3, devices=2, seq_len=8, block_len=0)}, "block_striped"),
+        ({"layout": N.BbLayout(kind=3, devices=4, seq_len=8, block_len=2)}, "block_striped"),
+        ({"mask": N.BbMask(kind=3, block_len=2, num_blocks=3, block_mask=8)}, "does not cover seq_len"),
+        ({"mask": N.BbMask(kind=2, window=0)}, "sliding_window"),
     ],
 )
 def test_abi_validates_before_cuda(over, msg):
