@@ -241,6 +241,14 @@ const char* bb_last_error(void);
 /* Diagnostics: with BB_PROBE=1 in the environment, kernels record per-phase
  * clock64() stamps of CTA (0,0) for its first tiles; copies n int64 to host. */
 int bb_debug_probe(int64_t* host_out, int32_t n);
+/* Mask realisation dump for tests (replaces nothing in the reference; it exposes what the
+ * kernels compute in place of local_pair_mask, partitioning.py:120-169).  For the ring step
+ * (q_device, k_device) with n_q query and n_k key rows, writes classes[qt * n_kt + kt]
+ * (device int8, 0 skip / 1 full / 2 partial) exactly as attn_fwd_kernel (view 0) or
+ * attn_bwd_kernel (view 1) classify the 128x128 tile, and, if `allowed` is not NULL,
+ * allowed[q * n_k + k] (device uint8, n_q x n_k) = the element mask that kernel applies. */
+int bb_debug_mask_tiles(const bb_layout* layout, const bb_mask* mask, int32_t q_device, int32_t k_device,
+                        int64_t n_q, int64_t n_k, int32_t view, int8_t* classes, uint8_t* allowed, void* stream);
 int32_t bb_abi_version(void);
 /* Number of kernel launches issued by this library since load (for bench). */
 int64_t bb_launch_count(void);

@@ -49,6 +49,7 @@ EXPORTS = (
     "bb_xent_f64",
     "bb_last_error",
     "bb_debug_probe",
+    "bb_debug_mask_tiles",
     "bb_abi_version",
     "bb_launch_count",
 )
@@ -180,6 +181,7 @@ def load(path: os.PathLike | str | None = None) -> C.CDLL:
     lib.bb_xent_f64.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp]
     lib.bb_last_error.restype = C.c_char_p
     lib.bb_debug_probe.argtypes = [vp, i32]
+    lib.bb_debug_mask_tiles.argtypes = [C.POINTER(BbLayout), C.POINTER(BbMask), i32, i32, i64, i64, i32, vp, vp, vp]
     lib.bb_abi_version.restype = i32
     lib.bb_launch_count.restype = i64
     for name in EXPORTS:

@@ -8,7 +8,9 @@ no CPU path: a CPU tensor, a wrong dtype or a missing library raises.
 from __future__ import annotations
 
 import ctypes as C
+import hashlib
 import math
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -55,13 +57,25 @@ class DeviceMask:
     spans: torch.Tensor | None = None
 
 
-_mask_cache: dict[tuple[int, int], DeviceMask] = {}
+_MASK_CACHE_SIZE = 16
+_mask_cache: "OrderedDict[tuple, DeviceMask]" = OrderedDict()
+
+
+def _mask_key(mask: MaskSpec, dev_index: int) -> tuple:
+    """Content key: a MaskSpec edited in place, or a new one with equal contents, maps to the
+    device copy of exactly those contents (never a stale one)."""
+    bm = None
+    if mask.kind == BLOCK_SPARSE and mask.block_mask is not None:
+        a = np.ascontiguousarray(np.asarray(mask.block_mask) != 0)
+        bm = (a.shape, hashlib.blake2b(a.tobytes(), digest_size=16).digest())
+    return (mask.kind, mask.window, mask.block_len, bm, dev_index)
 
 
 def device_mask(mask: MaskSpec, device: torch.device) -> DeviceMask:
-    key = (id(mask), device.index if device.index is not None else torch.cuda.current_device())
+    key = _mask_key(mask, device.index if device.index is not None else torch.cuda.current_device())
     hit = _mask_cache.get(key)
-    if hit is not None and hit.spec is mask:
+    if hit is not None:
+        _mask_cache.move_to_end(key)
         return hit
     bm = spans = None
     s = N.BbMask(kind=N.MASK_CODES[mask.kind], reserved=0, window=0, block_len=0, num_blocks=0, block_mask=None)
@@ -78,6 +92,8 @@ def device_mask(mask: MaskSpec, device: torch.device) -> DeviceMask:
         s.col_span = spans.data_ptr() + m.shape[0] * 2 * 4
     dm = DeviceMask(mask, s, bm, spans)
     _mask_cache[key] = dm
+    while len(_mask_cache) > _MASK_CACHE_SIZE:  # bounded: device copies of old masks are released
+        _mask_cache.popitem(last=False)
     return dm
 
 
@@ -200,6 +216,22 @@ def lmhead_fused(
         loss=_ptr(loss), dh=_ptr(dh), dw=_ptr(dw), workspace=_ptr(workspace), workspace_bytes=workspace.numel(),
     )
     N.check(N.load().bb_lmhead_fused(C.byref(a), C.c_void_p(_stream(h.device))))
+
+
+def debug_mask_tiles(layout: ShardLayout, mask: DeviceMask, q_device: int, k_device: int, n_q: int, n_k: int,
+                     view: str, device: torch.device) -> tuple[np.ndarray, np.ndarray]:
+    """The tile classes ([n_q/128, n_k/128] int8: 0 skip, 1 full, 2 partial) and the element
+    mask ([n_q, n_k] bool) that the forward (``view="fwd"``) or backward (``"bwd"``) kernel
+    realises for ring step (q_device, k_device); see bb_debug_mask_tiles."""
+    n_qt, n_kt = -(-n_q // 128), -(-n_k // 128)
+    cls = torch.zeros(n_qt * n_kt, dtype=torch.int8, device=device)
+    allowed = torch.zeros(n_q * n_k, dtype=torch.uint8, device=device)
+    lay = layout_struct(layout)
+    with torch.cuda.device(device):
+        N.check(N.load().bb_debug_mask_tiles(C.byref(lay), C.byref(mask.struct), q_device, k_device, n_q, n_k,
+                                             {"fwd": 0, "bwd": 1}[view], _ptr(cls), _ptr(allowed),
+                                             C.c_void_p(_stream(device))))
+    return cls.cpu().numpy().reshape(n_qt, n_kt), allowed.cpu().numpy().reshape(n_q, n_k).astype(bool)
 
 
 def padded_head_dim(d: int) -> int:

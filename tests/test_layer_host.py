@@ -29,3 +29,23 @@ def test_shard_row_map_inverts_the_shard_gather(kind, n, g, bl):
     shard_major = np.concatenate([np.asarray(ids) - 1 for ids in shard_token_arrays(layout)])
     assert sorted(rmap.tolist()) == list(range(n))
     assert np.array_equal(rmap[shard_major], np.arange(n))
+
+
+def test_attention_backward_checks_shapes_before_the_device():
+    """The reference raises for these through masked_scores / its matmuls (oracle.py:66-75,
+    98-119); the kernel path must raise before reading device memory out of bounds."""
+    from paper_2509_19836_b200.layer import attention_backward
+    from paper_2509_19836_b200.masks import block_sparse_mask, causal_mask
+
+    q, k, v, o, do = (np.zeros((8, 16)) for _ in range(5))
+    lse = np.zeros(8)
+    with pytest.raises(ValueError, match="Q has dim 16 but K has dim 8"):
+        attention_backward(q, np.zeros((8, 8)), v, o, lse, do, causal_mask())
+    with pytest.raises(ValueError, match="K has 8 rows but V has 4"):
+        attention_backward(q, k, np.zeros((4, 16)), o, lse, do, causal_mask())
+    with pytest.raises(ValueError, match="O must be 8x16"):
+        attention_backward(q, k, v, np.zeros((4, 16)), lse, do, causal_mask())
+    with pytest.raises(ValueError, match="lse must have 8 entries"):
+        attention_backward(q, k, v, o, np.zeros(5), do, causal_mask())
+    with pytest.raises(ValueError, match="block_mask must be 2x2"):  # mask smaller than the sequence
+        attention_backward(q, k, v, o, lse, do, block_sparse_mask(np.ones((1, 1)), 4))
