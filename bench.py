@@ -65,7 +65,11 @@ def parse():
     ap.add_argument("--ce-fanout", type=int, default=None, help="ce transport: copy streams per push (default BB_CE_FANOUT or 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-lmhead", action="store_true", help="skip the cfg5 fused LM-head sub-measurement")
+    ap.add_argument("--lm-tokens", type=int, default=131072, help="cfg5: tokens per GPU (2^20 over 8 GPUs)")
+    ap.add_argument("--lm-vocab", type=int, default=131072)
+    ap.add_argument("--lm-dim", type=int, default=4096)
+    ap.add_argument("--lm-rows", type=int, default=8192, help="cfg5: B_s row tile")
     return ap.parse_args()
 
 
@@ -126,61 +130,98 @@ class ClockSampler:
 # --------------------------------------------------------------------------- CPU oracle leg
 
 
+CPU_SAMPLE_SEQ = 4096  # the CPU leg's timed shape (per head): both arms report this sample
+CPU_FIT_SEQS = (1024, 2048, 4096)
+
+
 def _oracle_sample(args_tuple):
-    """One head of the reference algorithm (ring fwd + burst bwd, fp64) on a sub-sequence."""
+    """One head of the reference algorithm (ring fwd + burst bwd, fp64) on a sub-sequence,
+    single-threaded BLAS (one head per core).  Returns (pairs, seconds)."""
     n, d, g, seed = args_tuple
     import numpy as np
+    from threadpoolctl import threadpool_limits
 
     from oracle import burst_oracle as O
 
     rng = np.random.default_rng(seed)
     q, k, v, do = (rng.uniform(-1, 1, (n, 1, d)) for _ in range(4))
-    O.mh_ring_attention(q, k, v, do, ("zigzag", n, g, None), ("causal", None, None, None), O.ring_visit(1, g), backward="burst")
-    return n * (n + 1) // 2
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        O.mh_ring_attention(q, k, v, do, ("zigzag", n, g, None), ("causal", None, None, None), O.ring_visit(1, g),
+                            backward="burst")
+        return n * (n + 1) // 2, time.perf_counter() - t0
 
 
-def cpu_oracle_rate(d: int, cores: int, target_s: float, n: int = 2048, g: int = 4) -> dict:
-    """Time the oracle on `cores` processes (one head each) over ~target_s seconds; FLOP/s in the
-    same 14*d*P convention as the GPU number."""
+def cpu_sample_config(d: int, cores: int, g: int = 4) -> dict:
+    return {"seq": CPU_SAMPLE_SEQ, "simulated_ranks": g, "layout": "zigzag", "mask": "causal", "head_dim": d,
+            "heads_per_round": cores, "passes": "ring forward + burst backward", "arithmetic": "fp64 NumPy"}
+
+
+def cpu_round(ex, n: int, d: int, cores: int, g: int = 4, seed: int = 100) -> tuple[float, float]:
+    """One pool round: `cores` heads of sequence n, one per process.  (TFLOP/s, wall seconds)."""
+    t0 = time.perf_counter()
+    res = list(ex.map(_oracle_sample, [(n, d, g, seed + i) for i in range(cores)]))
+    dt = time.perf_counter() - t0
+    return 14.0 * d * sum(r[0] for r in res) / dt / 1e12, dt
+
+
+def cpu_oracle_fit(d: int, cores: int, cfg_seq: int, cfg_heads: int, g: int = 4) -> dict:
+    """The reference algorithm on this host's cores at N in CPU_FIT_SEQS (one head per core per
+    round), a least-squares fit seconds_per_head = c * N^2 through the points, and the fit
+    extrapolated to the GPU workload (labelled as such: the reference materialises n x n fp64
+    score matrices per ring step and cannot run it)."""
     import concurrent.futures as cf
 
-    t0 = time.perf_counter()
-    done_pairs = 0
-    heads = 0
+    points = []
     with cf.ProcessPoolExecutor(max_workers=cores) as ex:
-        while True:
-            pairs = list(ex.map(_oracle_sample, [(n, d, g, 100 + heads + i) for i in range(cores)]))
-            done_pairs += sum(pairs)
-            heads += cores
-            if time.perf_counter() - t0 >= target_s:
-                break
-    dt = time.perf_counter() - t0
-    flops = 14.0 * d * done_pairs
+        cpu_round(ex, 512, d, cores, g)  # worker start-up and imports, untimed
+        for n in CPU_FIT_SEQS:
+            rate, dt = cpu_round(ex, n, d, cores, g)
+            points.append({"seq": n, "heads": cores, "wall_s": round(dt, 3), "tflops": rate})
+    c = sum(p["wall_s"] * p["seq"] ** 2 for p in points) / sum(p["seq"] ** 4 for p in points)
+    per_head = c * cfg_seq ** 2
+    whole = per_head * cfg_heads / cores
+    pairs = cfg_seq * (cfg_seq + 1) // 2
+    sample = next(p for p in points if p["seq"] == CPU_SAMPLE_SEQ)
     return {
-        "value": flops / dt / 1e12,
+        "value": sample["tflops"],
         "unit": "TFLOPS",
         "cores": cores,
-        "seconds": round(dt, 2),
-        "sample": f"oracle (reference algorithm, fp64 NumPy einsum) ring fwd + burst bwd, zigzag causal, "
-        f"seq {n}, G={g} simulated ranks, d={d}, {heads} heads over {cores} processes",
+        "kind": "port",
+        "seconds": round(sum(p["wall_s"] for p in points), 2),
+        "sample": f"oracle (reference algorithm, fp64 NumPy) ring fwd + burst bwd, zigzag causal, seq {CPU_SAMPLE_SEQ}, "
+        f"G={g} simulated ranks, d={d}, {cores} heads on {cores} processes (one per core)",
+        "sample_config": cpu_sample_config(d, cores, g),
+        "fit": {
+            "model": "wall seconds per round (one head per core) = c * N^2, least squares over the measured points",
+            "c": c,
+            "points": points,
+            "extrapolated": {"label": "extrapolation, not a measurement", "seq": cfg_seq, "heads": cfg_heads,
+                             "seconds": whole, "tflops": 14.0 * d * cfg_heads * pairs / whole / 1e12},
+        },
     }
 
 
 def run_reference(args, rank: int, world: int) -> None:
-    """--impl reference: the reference's CPU algorithm (oracle port) on this box's host cores."""
+    """--impl reference: the reference's CPU algorithm (oracle port) on this box's host cores.
+    A step is one pool round of the CPU sample (CPU_SAMPLE_SEQ, one head per core); the line
+    also carries the N^2 fit the GPU arm's cpu_baseline reports, from the same function."""
     if rank != 0:
         return
+    import concurrent.futures as cf
+
     cores = os.cpu_count() or 1
-    # warmup + timed samples, each sample ~ one pool round
-    for _ in range(max(0, args.warmup)):
-        cpu_oracle_rate(args.head_dim, cores, 0.0)
-    t = []
-    rates = []
-    for _ in range(max(1, args.steps)):
-        r = cpu_oracle_rate(args.head_dim, cores, 0.0)
-        t.append(r["seconds"])
-        rates.append(r["value"])
+    d = args.head_dim
+    rates, t = [], []
+    with cf.ProcessPoolExecutor(max_workers=cores) as ex:
+        for _ in range(max(0, args.warmup)):
+            cpu_round(ex, CPU_SAMPLE_SEQ, d, cores)
+        for i in range(max(1, args.steps)):
+            r, dt = cpu_round(ex, CPU_SAMPLE_SEQ, d, cores, seed=1000 + i * cores)
+            rates.append(r)
+            t.append(dt)
     value = statistics.median(rates)
+    fit = cpu_oracle_fit(d, cores, args.seq, args.heads)
     line = {
         "impl": "reference",
         "metric": "BurstAttention fwd+bwd TFLOPS/GPU & MFU at 1M tokens, 1/2/4/8 B200",
@@ -196,16 +237,17 @@ def run_reference(args, rank: int, world: int) -> None:
         "dtype": "f64",
         "data": "synthetic (uniform [-1,1])",
         "config": workload_config(args, world),
+        "sample_config": cpu_sample_config(d, cores),
         "cpu_baseline": {
             "value": value, "unit": "TFLOPS", "cores": cores, "kind": "port",
-            "sample": r["sample"] + " (reference arm: oracle port; burstsim itself is not on the GPU box)",
+            "sample": fit["sample"] + " (reference arm: oracle port; burstsim itself is not on the GPU box)",
+            "sample_config": cpu_sample_config(d, cores),
+            "fit": fit["fit"],
         },
+        "fit": fit["fit"],
         "e2e": {"value": value, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
-
-
-# --------------------------------------------------------------------------- GPU leg
 
 
 def make_mask(args):
@@ -456,6 +498,8 @@ def run_gpu(args) -> None:
             "pipelining": "H2D of step i+1 and D2H of step i on a side stream, overlapping step i; the forward starts once Q/K/V are up (dO lands during it)",
         }
 
+    lm = None if args.no_lmhead else run_lmhead(args, dev, world)
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -496,6 +540,8 @@ def run_gpu(args) -> None:
             "unit": "TFLOP/s",
             "frac": achieved / peak,
             "traffic": traffic,
+            "traffic_source": "profile-derived: dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full "
+            "capture of this kernel (profiles/roofline_traffic.json), not measured in this run",
             "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json)" if peak_src == "measured" else "fallback 1.4 PF sustained (B200_PROFILING.md)",
             "algorithmic_flops_per_launch": bwd_per_launch,
             "avg_launch_ms": avg_bwd * 1e3,
@@ -504,13 +550,71 @@ def run_gpu(args) -> None:
         "clocks": clk.summary(),
         "ring_bytes_sent_per_step_rank0": ring_bytes,
         "ring_overlap": overlap,
+        "lmhead": lm,
     }
+    if lm is not None:
+        lm["roofline"]["peak"] = peak
+        lm["roofline"]["frac"] = lm["roofline"]["achieved"] / peak
     if world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_oracle_rate(args.head_dim, 1, args.cpu_seconds)
-        line["cpu_baseline"]["kind"] = "port"
+        line["cpu_baseline"] = cpu_oracle_fit(args.head_dim, os.cpu_count() or 1, args.seq, args.heads)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_lmhead(args, dev, world: int) -> dict:
+    """cfg5 (BASELINE.json configs[4]): the fused LM head + cross entropy of a 2^20-token
+    sequence sharded over 8 GPUs -- each rank runs its 131072-token shard through
+    sharded_fused_lmhead_loss (V = 131072, D = 4096, W replicated, dW all-reduced over the
+    ranks, loss summed).  6*N*V*D FLOPs per shard (no logits recompute); CUDA
+    events on the launching stream, max over ranks."""
+    import math
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_19836_b200.lmhead import FusionConfig, sharded_fused_lmhead_loss
+
+    n, v, d = args.lm_tokens, args.lm_vocab, args.lm_dim
+    g = torch.Generator(device=dev).manual_seed(77 + (dist.get_rank() if world > 1 else 0))
+    h = (torch.rand(n, d, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
+    w = ((torch.rand(v, d, device=dev, generator=torch.Generator(device=dev).manual_seed(78)) * 2 - 1)
+         / math.sqrt(d)).to(torch.bfloat16)
+    y = torch.randint(0, v, (n,), device=dev, generator=g)
+    cfg = FusionConfig(args.lm_rows, 4096)
+    stream = torch.cuda.current_stream(dev)
+    sharded_fused_lmhead_loss(h, w, y, cfg)  # warm-up (workspace, descriptors)
+    torch.cuda.synchronize()
+    steps = 2
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    e0.record(stream)
+    for _ in range(steps):
+        res = sharded_fused_lmhead_loss(h, w, y, cfg)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / 1e3 / steps], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t = float(t.item())
+    flops = 6.0 * n * v * d
+    out = {
+        "workload": f"cfg5 fused LM head + CE: {n} tokens per GPU (2^20 over 8 GPUs), V={v}, D={d}, B_s={args.lm_rows}, "
+        "sum loss, dW all-reduced over the ranks",
+        "value": flops * world / t / 1e12,
+        "unit": "TFLOPS",
+        "ms_per_step": t * 1e3,
+        "tflops_per_gpu": flops / t / 1e12,
+        "total_loss": res.total_loss,
+        "roofline": {"kernel": "bb_lmhead_fused (3 tcgen05 GEMMs + LSE / softmax-onehot passes per row tile)",
+                     "bound": "tensor", "achieved": flops / t / 1e12, "unit": "TFLOP/s",
+                     "algorithmic_flops_per_launch": flops, "traffic": None},
+        "steps": steps,
+    }
+    del h, w, y, res
+    torch.cuda.empty_cache()
+    return out
 
 
 def _json_stdout():

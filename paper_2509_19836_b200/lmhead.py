@@ -103,6 +103,39 @@ def all_reduce_dw(dw: torch.Tensor, group=None) -> torch.Tensor:
     return dw
 
 
+@dataclass
+class ShardedLossResult:
+    """One rank's share of a sequence-sharded LM head: its tokens' losses
+    and dH rows, the dW summed over every shard, and the job's total (summed) loss."""
+
+    loss: torch.Tensor  # this shard's per-token nats
+    dh: torch.Tensor  # this shard's rows
+    dw: torch.Tensor  # [V, D], all-reduced: identical on every rank
+    total_loss: float  # sum over all shards' tokens (oracle.py:129-133 sums, never averages)
+    peak_aux_elements: int
+
+
+def sharded_fused_lmhead_loss(h_local: torch.Tensor, w_head: torch.Tensor, targets_local: torch.Tensor,
+                              cfg: FusionConfig, group=None) -> ShardedLossResult:
+    """The LM head of a sequence sharded over the ranks of ``group`` (one process per GPU, W
+    replicated): each rank runs the fused head on its own tokens, then dW is summed over the
+    shards (all_reduce_dw) and the per-token losses are summed into the job's loss.  Token
+    shards are independent in the forward and in dH (lmhead.py:41-93 is row-separable), so the
+    only exchange is dW and one scalar."""
+    import torch.distributed as dist
+
+    v, d = w_head.shape
+    dev = h_local.device
+    dw = torch.zeros(v, max(8, (d + 7) // 8 * 8), dtype=torch.float32, device=dev)
+    res = fused_lmhead_loss(h_local, w_head, targets_local, cfg, device=dev, dw_out=dw)
+    total = res.loss.double().sum().reshape(1)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(total, group=group)
+    all_reduce_dw(dw, group)
+    return ShardedLossResult(loss=res.loss, dh=res.dh, dw=dw[:, :d], total_loss=float(total.item()),
+                             peak_aux_elements=res.peak_aux_elements)
+
+
 def memory_footprint(n: int, vocab: int, dim: int, cfg: FusionConfig) -> tuple[int, int]:
     """(naive N*V, fused min(B_s, N)*V) logits-class elements (lmhead.py:96-110)."""
     if n < 1 or vocab < 1 or dim < 1:
