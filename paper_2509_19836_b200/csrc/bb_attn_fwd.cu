@@ -7,7 +7,7 @@
 // exp_gap weights of distributed.py:184-188 -- the merge is the epilogue.
 //
 // CTA = 2 query tiles of 128 rows x one head; K/V tiles of 128 keys stream
-// through a 3-slot TMA ring and are shared by both query tiles.
+// through a 5-slot TMA ring and are shared by both query tiles.
 //   warp 0      TMA producer (Q once, then K_j, V_j)
 //   warp 1      MMA issuer: S_k = Q_k K_j^T (SS, M=128,N=128) and
 //               O_k += P_k V_j (TS: P read from TMEM, V MN-major from smem) into TMEM
@@ -17,9 +17,11 @@
 //               lazy (threshold 8) rescale of the TMEM O accumulator, P (bf16)
 //               written back over its own S columns in TMEM (tcgen05.st), where the
 //               P.V MMA reads it as the A operand -- no shared-memory round trip.
-// Tiles are classified from the closed-form id bounds (bb_mask.cuh): fully
-// masked tiles are never loaded or multiplied, fully visible tiles skip the
-// per-element predicate.
+// Registers: setmaxnreg gives the softmax warpgroups 216 (S row in registers, no spills;
+// a spill here goes to L2, the 226 KB of shared memory leaves L1 ~2 KB) and the control
+// warpgroup 64.  Tiles are classified from the closed-form id bounds (bb_mask.cuh): fully
+// masked tiles are never loaded or multiplied, fully visible tiles skip the per-element
+// predicate.
 #include <cuda_runtime.h>
 
 #include <type_traits>
@@ -34,58 +36,24 @@ namespace {
 constexpr int FWD_THREADS = 384;
 constexpr int MAX_KT = 4096;  // key tiles per shard the class table holds (n_k <= 524288)
 constexpr int KV_SLOTS = 5;
-constexpr float RESCALE_THRESHOLD = 8.0f;
-#ifndef BB_POLY_EVERY
-#define BB_POLY_EVERY 1000  // measured: any FMA-pipe share of exp2 was slower on B200
+constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units: P may reach 2^8 before O is rescaled
+constexpr uint32_t REGS_CTRL = 64, REGS_SOFTMAX = 216;
+static_assert(REGS_CTRL * 128 + REGS_SOFTMAX * 256 <= 65536, "register budget");
+#ifndef BB_FWD_POLY
+// Every BB_FWD_POLY-th exponential pair of an unmasked tile goes to a cubic on the FMA pipe
+// (ex2_poly2) instead of MUFU (16 lanes/clk/SM: a 128x128 tile's exps need as many cycles as
+// its two MMAs).  0 = MUFU only.
+#define BB_FWD_POLY 0
 #endif
-#ifndef BB_FWD_REGS
-#define BB_FWD_REGS 0  // setmaxnreg split measured: ptxas then spills far more (1.8 KB)
-#endif
-#ifndef BB_FWD_REGS_LO
-#define BB_FWD_REGS_LO 88
-#endif
-#ifndef BB_FWD_REGS_HI
-#define BB_FWD_REGS_HI 208
-#endif
-#ifndef BB_FWD_X2
-#define BB_FWD_X2 1
-#endif
-#ifndef BB_PACK_INT
-#define BB_PACK_INT 0
-#endif
-#ifndef BB_FWD_CHUNKED
-// S read from TMEM in 32-column chunks twice (row max, then exp) instead of held whole in
-// registers: s[128] per thread spilled ~230 B to local memory at the 168-register budget.
-#define BB_FWD_CHUNKED 0  // measured 10 % slower (1162 -> 1050 TF/s full 32K): the second TMEM pass costs more than the spills
-#endif
-#ifndef BB_FWD_SPLIT
-// Two softmax threads per query row (640 threads: 4 softmax warps per SMSP), each owning 64
-// of the 128 key columns: P of keys [64h, 64h+64) lands in S columns [64h, 64h+32), the row
-// max is exchanged through shared memory once per tile, S is re-read for the exp pass.
-#define BB_FWD_SPLIT 0  // measured 5 % slower (1110 vs 1165 TF/s full 32K, 995 vs 1039 causal 128K); parity-tested
-#endif
-#ifndef BB_SPLIT_POLY
-#define BB_SPLIT_POLY 0
-#endif
-#ifndef BB_FWD_PINGPONG
-#define BB_FWD_PINGPONG 0  // softmax warpgroups take turns on MUFU (named barriers 1, 2): measured 16 % slower (1159 -> 972 TF/s full 32K)
-#endif
-constexpr int POLY_EVERY = BB_POLY_EVERY;  // every POLY_EVERY-th P column uses ex2_poly (>8: never)  // log2 units: P may reach 2^8 before O is rescaled
 
-template <bool SPLIT>
-constexpr int fwd_threads() { return SPLIT ? 640 : FWD_THREADS; }
-template <bool SPLIT>
-constexpr int kv_slots() { return SPLIT ? 4 : KV_SLOTS; }
-
-template <int D, bool SPLIT = false>
+template <int D>
 struct FwdSmem {
   static constexpr uint32_t TILE = 128 * D * 2;  // one Q / K / V tile, D/64 panels of 16 KB
   static constexpr uint32_t Q_OFF = 0;
   static constexpr uint32_t KV_OFF = Q_OFF + 2 * TILE;
-  static constexpr uint32_t BAR_OFF = KV_OFF + kv_slots<SPLIT>() * TILE;
+  static constexpr uint32_t BAR_OFF = KV_OFF + KV_SLOTS * TILE;
   static constexpr uint32_t CLS_OFF = BAR_OFF + 256;  // per key tile: class(q tile 0) | class(q tile 1) << 2
-  static constexpr uint32_t XCH_OFF = CLS_OFF + MAX_KT / 2;  // SPLIT: [parity][q tile][half][row] floats
-  static constexpr uint32_t BYTES = XCH_OFF + (SPLIT ? 2 * 2 * 2 * 128 * 4 : 0);
+  static constexpr uint32_t BYTES = CLS_OFF + MAX_KT / 2;
 };
 
 struct FwdParams {
@@ -114,186 +82,12 @@ __device__ __forceinline__ int32_t fwd_class(const FwdParams& p, int q, int64_t 
   return classify_tile(p.layout, p.mask, p.q_device, r0, r1, p.k_device, c0, c1, c1 - c0 == 128);
 }
 
-// Softmax / correction / epilogue with two threads per query row (SPLIT): thread (q, h, row)
-// owns key columns [64h, 64h+64) of S and output columns [h*D/2, (h+1)*D/2) of O.
-template <int D, typename ClsFn>
-__device__ __forceinline__ void fwd_softmax_split(const FwdParams& p, uint8_t* xch_smem, uint32_t tmem, uint64_t* s_full,
-                                                  uint64_t* p_full, uint64_t* pv_done, int64_t m0, int64_t j_lo,
-                                                  int64_t j_hi, int head, ClsFn tile_cls) {
-  const uint32_t warp = warp_id(), lane = lane_id();
-  const int sw = static_cast<int>(warp) - 4;
-  const int q = sw >> 3, half = (sw >> 2) & 1;
-  const uint32_t quad = warp & 3;
-  const int row = quad * 32 + lane;
-  const int64_t qrow = m0 + 128 * q + row;
-  const bool row_ok = qrow < p.n_q;
-  const int64_t q_id = row_ok ? token_id(p.layout, p.q_device, qrow) : 0;
-  const uint32_t t_lane = (quad * 32) << 16;
-  const uint32_t s_col = tmem + t_lane + q * 128u + 64u * half;   // my 64 S columns
-  const uint32_t o_col = tmem + t_lane + 256u + q * D + (D / 2) * half;  // my D/2 O columns
-  float* xch = reinterpret_cast<float*>(xch_smem);  // [parity][q][half][row]
-  auto xslot = [&](uint32_t par, int hh) -> float& { return xch[((par * 2 + q) * 2 + hh) * 128 + row]; };
-  const float sl2 = p.scale_log2;
-  const uint32_t bar_id = 1 + q;  // the 256 threads of this query tile
-
-  float m_run = -INFINITY, l_run = 0.f;
-  uint32_t t = 0;
-  for (int64_t j = j_lo; j < j_hi; ++j) {
-    const int32_t cls = tile_cls(q, j);
-    if (cls == TILE_SKIP) continue;
-    if (row == 0 && half == 0) FWD_PROBE(t, 16 + 8 * q);
-    mbar_wait(&s_full[q], t & 1);
-    if (row == 0 && half == 0) FWD_PROBE(t, 17 + 8 * q);
-    tc_fence_after();
-    uint4 bits = make_uint4(~0u, ~0u, ~0u, ~0u);
-    if (cls == TILE_PARTIAL) bits = row_mask_bits(p.layout, p.mask, q_id, row_ok, p.k_device, j * 128, p.n_k, true);
-    float ca[32], cb[32];
-    auto mask32 = [&](float(&x)[32], int c0) {
-#pragma unroll
-      for (int c = 0; c < 32; ++c)
-        if (!mask_bit(bits, c0 + c)) x[c] = -INFINITY;
-    };
-    tmem_ld32(s_col, ca);
-    tmem_ld32(s_col + 32, cb);
-    tmem_ld_wait();
-    reg_fence(ca);
-    reg_fence(cb);
-    if (cls == TILE_PARTIAL) {
-      mask32(ca, 64 * half);
-      mask32(cb, 64 * half + 32);
-    }
-    float mx8[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) mx8[i] = fmax3(fmax3(ca[i], ca[i + 8], ca[i + 16]), fmax3(ca[i + 24], cb[i], cb[i + 8]), fmaxf(cb[i + 16], cb[i + 24]));
-    const float m_half = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
-    xslot(t & 1, half) = m_half;
-    if (row == 0 && half == 0) FWD_PROBE(t, 23 + 8 * q);
-    named_bar_sync(bar_id, 256);
-    if (row == 0 && half == 0) FWD_PROBE(t, 22 + 8 * q);
-    const float mx = fmaxf(m_half, xslot(t & 1, half ^ 1));
-    const float m_tile = mx * sl2;
-    const bool need = m_tile > m_run + RESCALE_THRESHOLD;  // identical in both halves of the row
-    float alpha = 1.f;
-    if (need) {
-      alpha = (m_run == -INFINITY) ? 0.f : ex2_approx(m_run - m_tile);
-      m_run = m_tile;
-      l_run *= alpha;
-    }
-    const float neg_m = (m_run == -INFINITY) ? 0.f : -m_run;
-    if (t > 0) {
-      mbar_wait(&pv_done[q], (t - 1) & 1);
-      if (row == 0 && half == 0) FWD_PROBE(t, 18 + 8 * q);
-      tc_fence_after();
-      if (__any_sync(0xffffffff, need)) {
-#pragma unroll 1
-        for (int c = 0; c < D / 64; ++c) {
-          float o[32];
-          tmem_ld32(o_col + c * 32, o);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] *= alpha;
-          tmem_st32(o_col + c * 32, o);
-        }
-        tmem_st_wait();
-      }
-    }
-    // exp pass: P of keys [64h, 64h+64) -> columns [64h, 64h+32) of this S region, which only
-    // this thread reads
-    float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-    const float2 sl2x2 = make_float2(sl2, sl2), negm2 = make_float2(neg_m, neg_m);
-    const bool poly_ok = cls != TILE_PARTIAL;  // masked -inf scores need MUFU's exact 0
-    auto exp32 = [&](const float(&x)[32], uint32_t dst) {
-      uint32_t pk[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float2 y = __ffma2_rn(make_float2(x[2 * i], x[2 * i + 1]), sl2x2, negm2);
-        // BB_SPLIT_POLY: every 4th pair on the FMA pipe (MUFU alone needs as many cycles per
-        // key tile as the tile's MMAs)
-        const float2 e = (BB_SPLIT_POLY && (i & 3) == 3 && poly_ok) ? ex2_poly2(y)
-                                                                     : make_float2(ex2_approx(y.x), ex2_approx(y.y));
-        acc4[i & 3] = __fadd2_rn(acc4[i & 3], e);
-        pk[i] = pack_bf16(e.x, e.y);
-      }
-      tmem_st16(dst, pk);
-    };
-    // S is re-read rather than kept live across the exchange barrier (96-register budget)
-    tmem_ld32(s_col, ca);
-    tmem_ld32(s_col + 32, cb);
-    tmem_ld_wait();
-    reg_fence(ca);
-    reg_fence(cb);
-    if (cls == TILE_PARTIAL) {
-      mask32(ca, 64 * half);
-      mask32(cb, 64 * half + 32);
-    }
-    exp32(ca, s_col);
-    exp32(cb, s_col + 16);
-    if (row == 0 && half == 0) FWD_PROBE(t, 20 + 8 * q);
-    l_run += ((acc4[0].x + acc4[0].y) + (acc4[1].x + acc4[1].y)) + ((acc4[2].x + acc4[2].y) + (acc4[3].x + acc4[3].y));
-    tmem_st_wait();
-    tc_fence_before();
-    mbar_arrive(&p_full[q]);
-    if (row == 0 && half == 0) FWD_PROBE(t, 19 + 8 * q);
-    ++t;
-  }
-
-  if (t > 0) {
-    float* lse_ptr = p.lse + static_cast<int64_t>(head) * p.n_q + qrow;
-    const float lse_prev = row_ok ? *lse_ptr : -INFINITY;  // read by both halves before half 0 writes
-    xslot(t & 1, half) = l_run;
-    named_bar_sync(bar_id, 256);
-    const float l_tot = l_run + xslot(t & 1, half ^ 1);
-    mbar_wait(&pv_done[q], (t - 1) & 1);
-    tc_fence_after();
-    const float lse_step = (l_tot > 0.f) ? (m_run * 0.69314718055994531f + logf(l_tot)) : -INFINITY;
-    float w_step = 0.f, w_old = 0.f, lse_new = -INFINITY;
-    const bool write = row_ok && lse_step != -INFINITY;
-    if (write) {
-      if (lse_prev == -INFINITY) {
-        lse_new = lse_step;
-        w_step = 1.f / l_tot;
-      } else {
-        const float hi = fmaxf(lse_prev, lse_step), lo = fminf(lse_prev, lse_step);
-        lse_new = hi + log1pf(expf(lo - hi));
-        w_step = expf(lse_step - lse_new) / l_tot;
-        w_old = expf(lse_prev - lse_new);
-      }
-    }
-    named_bar_sync(bar_id, 256);  // both halves have read lse_prev
-    if (write && half == 0) *lse_ptr = lse_new;
-    float* o_row = p.o + (qrow * p.hq + head) * static_cast<int64_t>(D) + (D / 2) * half;
-#pragma unroll 1
-    for (int c = 0; c < D / 64; ++c) {
-      float o[32];
-      tmem_ld32(o_col + c * 32, o);
-      tmem_ld_wait();
-      if (write) {
-        float4* dst = reinterpret_cast<float4*>(o_row + c * 32);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          float4 r = make_float4(o[4 * i] * w_step, o[4 * i + 1] * w_step, o[4 * i + 2] * w_step, o[4 * i + 3] * w_step);
-          if (w_old != 0.f) {
-            const float4 prev = dst[i];
-            r.x += w_old * prev.x;
-            r.y += w_old * prev.y;
-            r.z += w_old * prev.z;
-            r.w += w_old * prev.w;
-          }
-          dst[i] = r;
-        }
-      }
-    }
-  }
-}
-
-template <int D, bool SPLIT>
-__global__ void __launch_bounds__(fwd_threads<SPLIT>(), 1)
+template <int D>
+__global__ void __launch_bounds__(FWD_THREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                     const __grid_constant__ CUtensorMap tv, const __grid_constant__ FwdParams p) {
-  using L = FwdSmem<D, SPLIT>;
+  using L = FwdSmem<D>;
   constexpr int PANELS = D / 64;
-  constexpr int KV_SLOTS = kv_slots<SPLIT>();
-  constexpr int FWD_THREADS = fwd_threads<SPLIT>();
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023) != 0) __trap();
 
@@ -325,7 +119,7 @@ __global__ void __launch_bounds__(fwd_threads<SPLIT>(), 1)
     }
     for (int k = 0; k < 2; ++k) {
       mbar_init(&s_full[k], 1);
-      mbar_init(&p_full[k], SPLIT ? 256 : 128);
+      mbar_init(&p_full[k], 128);
       mbar_init(&pv_done[k], 1);
     }
     fence_barrier_init();
@@ -342,141 +136,132 @@ __global__ void __launch_bounds__(fwd_threads<SPLIT>(), 1)
     }
     cls_tab[b] = static_cast<uint8_t>(byte);
   }
-  auto tile_nib = [&](int64_t jj) {
+  auto tile_nib = [&](int64_t jj) {  // class(q tile 0) | class(q tile 1) << 2 of key tile jj
     const int64_t x = jj - j_lo;
     return static_cast<uint32_t>(cls_tab[x >> 1] >> (4 * (x & 1))) & 15u;
   };
-  auto tile_cls = [&](int q, int64_t jj) { return static_cast<int32_t>((tile_nib(jj) >> (2 * q)) & 3); };
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-#if BB_FWD_REGS
-  // producer / MMA warpgroup gives registers to the two softmax warpgroups (s[128] + P)
-  if (warp < 4)
-    setmaxnreg_dec<BB_FWD_REGS_LO>();
-  else
-    setmaxnreg_inc<BB_FWD_REGS_HI>();
-#endif
 
-  if (warp == 0) {
-    // ------------------------------------------------ TMA producer
-    if (elect_one()) {
-      const bool q1_live = m0 + 128 < p.n_q;
-      mbar_expect_tx(q_full, (q1_live ? 2 : 1) * L::TILE);
-      for (int q = 0; q < (q1_live ? 2 : 1); ++q)
-        for (int pn = 0; pn < PANELS; ++pn)
-          tma_load_2d(smem + L::Q_OFF + q * L::TILE + pn * 16384, &tq, q_full, head * D + pn * 64,
-                      static_cast<int32_t>(m0 + 128 * q));
-      uint32_t use = 0;
-      for (int64_t j = j_lo; j < j_hi; ++j) {
-        if (tile_nib(j) == 0) continue;  // both query tiles skip
-        for (int which = 0; which < 2; ++which, ++use) {
-          const uint32_t s = use % KV_SLOTS, ph = (use / KV_SLOTS) & 1;
-          FWD_PROBE(use >> 1, 0 + which * 2);
-          mbar_wait(&kv_empty[s], ph ^ 1);
-          FWD_PROBE(use >> 1, 1 + which * 2);
-          mbar_expect_tx(&kv_full[s], L::TILE);
+  if (warp < 4) {
+    setmaxnreg_dec<REGS_CTRL>();
+    if (warp == 0) {
+      // ------------------------------------------------ TMA producer
+      if (elect_one()) {
+        const bool q1_live = m0 + 128 < p.n_q;
+        mbar_expect_tx(q_full, (q1_live ? 2 : 1) * L::TILE);
+        for (int q = 0; q < (q1_live ? 2 : 1); ++q)
           for (int pn = 0; pn < PANELS; ++pn)
-            tma_load_2d(smem + L::KV_OFF + s * L::TILE + pn * 16384, which ? &tv : &tk, &kv_full[s],
-                        kv_head * D + pn * 64, static_cast<int32_t>(j * 128));
+            tma_load_2d(smem + L::Q_OFF + q * L::TILE + pn * 16384, &tq, q_full, head * D + pn * 64,
+                        static_cast<int32_t>(m0 + 128 * q));
+        uint32_t use = 0;
+        for (int64_t j = j_lo; j < j_hi; ++j) {
+          if (tile_nib(j) == 0) continue;  // both query tiles skip
+          for (int which = 0; which < 2; ++which, ++use) {
+            const uint32_t s = use % KV_SLOTS, ph = (use / KV_SLOTS) & 1;
+            FWD_PROBE(use >> 1, 0 + which * 2);
+            mbar_wait(&kv_empty[s], ph ^ 1);
+            FWD_PROBE(use >> 1, 1 + which * 2);
+            mbar_expect_tx(&kv_full[s], L::TILE);
+            for (int pn = 0; pn < PANELS; ++pn)
+              tma_load_2d(smem + L::KV_OFF + s * L::TILE + pn * 16384, which ? &tv : &tk, &kv_full[s],
+                          kv_head * D + pn * 64, static_cast<int32_t>(j * 128));
+          }
         }
       }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
-    // Order per active kv tile j (jn = next active tile):  PV0(j), S0(jn), PV1(j), S1(jn).
-    // S0(jn) only needs softmax 0 to have consumed S0(j) (it has: P0(j) is ready), so
-    // query tile 0's softmax of jn overlaps PV1(j) and S1(jn) overlaps softmax 1 -- the
-    // tensor pipe never waits on both softmax groups at once.
-    constexpr uint32_t idesc_s = idesc_bf16(128, 128, false, false);
-    constexpr uint32_t idesc_o = idesc_bf16(128, D, false, true);
-    uint32_t issued[2] = {0, 0};
-    auto kv_slot = [](uint32_t use) { return use % KV_SLOTS; };
-    auto kv_par = [](uint32_t use) { return (use / KV_SLOTS) & 1; };
-    auto issue_s = [&](int q, uint32_t k_base) {
-      if (elect_one()) {
-        const uint32_t q_base = smem_u32(smem + L::Q_OFF + q * L::TILE);
+    } else if (warp == 1) {
+      // ------------------------------------------------ MMA issuer
+      // Order per active kv tile j (jn = next active tile):  PV0(j), S0(jn), PV1(j), S1(jn).
+      // S0(jn) only needs softmax 0 to have consumed S0(j) (it has: P0(j) is ready), so
+      // query tile 0's softmax of jn overlaps PV1(j) and S1(jn) overlaps softmax 1 -- the
+      // tensor pipe never waits on both softmax groups at once.
+      constexpr uint32_t idesc_s = idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idesc_o = idesc_bf16(128, D, false, true);
+      uint32_t issued0 = 0, issued1 = 0;
+      auto kv_slot = [](uint32_t use) { return use % KV_SLOTS; };
+      auto kv_par = [](uint32_t use) { return (use / KV_SLOTS) & 1; };
+      auto issue_s = [&](int q, uint32_t k_base) {
+        if (elect_one()) {
+          const uint32_t q_base = smem_u32(smem + L::Q_OFF + q * L::TILE);
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
-          umma_ss(tmem + (q * 128u), sw128_desc(q_base + off, 16, 1024), sw128_desc(k_base + off, 16, 1024),
-                  idesc_s, ks > 0);
+          for (int ks = 0; ks < D / 16; ++ks) {
+            const uint32_t off = (ks >> 2) * 16384 + (ks & 3) * 32;
+            umma_ss(tmem + (q * 128u), sw128_desc(q_base + off, 16, 1024), sw128_desc(k_base + off, 16, 1024),
+                    idesc_s, ks > 0);
+          }
+          umma_commit(&s_full[q]);
         }
-        umma_commit(&s_full[q]);
-      }
-      __syncwarp();
-    };
-    auto issue_pv = [&](int q, uint32_t v_base) {
-      mbar_wait(&p_full[q], issued[q] & 1);
-      tc_fence_after();
-      if (elect_one()) {
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {  // A = P: 16 keys (8 packed columns) per k-step
-          const uint64_t bd = sw128_desc(v_base + ks * 2048, 16384, 1024);
-          // P of 16 keys = 8 packed columns; SPLIT keeps keys [64h, 64h+64) in columns [64h, 64h+32)
-          const uint32_t pcol = SPLIT ? (ks < 4 ? ks * 8u : 64u + (ks - 4) * 8u) : ks * 8u;
-          umma_ts(tmem + (256u + q * D), tmem + q * 128u + pcol, bd, idesc_o, (issued[q] | ks) != 0);
-        }
-        umma_commit(&pv_done[q]);
-      }
-      __syncwarp();
-      ++issued[q];
-    };
-    auto next_active = [&](int64_t from, int32_t* c) {
-      for (int64_t jj = from; jj < j_hi; ++jj) {
-        c[0] = tile_cls(0, jj);
-        c[1] = tile_cls(1, jj);
-        if (c[0] != TILE_SKIP || c[1] != TILE_SKIP) return jj;
-      }
-      return j_hi;
-    };
-    mbar_wait(q_full, 0);
-    int32_t cls[2], cls_n[2];
-    int64_t j = next_active(j_lo, cls);
-    if (j < j_hi) {  // prologue: S of the first active tile
-      mbar_wait(&kv_full[kv_slot(0)], kv_par(0));
-      tc_fence_after();
-      const uint32_t k_base = smem_u32(smem + L::KV_OFF + kv_slot(0) * L::TILE);
-      for (int q = 0; q < 2; ++q)
-        if (cls[q] != TILE_SKIP) issue_s(q, k_base);
-      if (elect_one()) umma_commit(&kv_empty[kv_slot(0)]);
-      __syncwarp();
-    }
-    for (uint32_t t = 0; j < j_hi; ++t) {
-      const int64_t jn = next_active(j + 1, cls_n);
-      const uint32_t uv = 2 * t + 1, uk = 2 * t + 2;
-      if (lane == 0) FWD_PROBE(t, 4);
-      mbar_wait(&kv_full[kv_slot(uv)], kv_par(uv));
-      if (lane == 0) FWD_PROBE(t, 5);
-      tc_fence_after();
-      const uint32_t v_base = smem_u32(smem + L::KV_OFF + kv_slot(uv) * L::TILE);
-      const uint32_t kn_base = smem_u32(smem + L::KV_OFF + kv_slot(uk) * L::TILE);
-      if (cls[0] != TILE_SKIP) issue_pv(0, v_base);
-      if (lane == 0) FWD_PROBE(t, 7);
-      if (jn < j_hi) {
-        mbar_wait(&kv_full[kv_slot(uk)], kv_par(uk));
+        __syncwarp();
+      };
+      auto issue_pv = [&](int q, uint32_t v_base, uint32_t& issued) {
+        mbar_wait(&p_full[q], issued & 1);
         tc_fence_after();
-        if (cls_n[0] != TILE_SKIP) issue_s(0, kn_base);
-      }
-      if (cls[1] != TILE_SKIP) issue_pv(1, v_base);
-      if (lane == 0) FWD_PROBE(t, 9);
-      if (jn < j_hi) {
-        if (cls_n[1] != TILE_SKIP) issue_s(1, kn_base);
-        if (elect_one()) umma_commit(&kv_empty[kv_slot(uk)]);
+        if (elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)  // A = P: 16 keys (8 packed columns) per k-step
+            umma_ts(tmem + (256u + q * D), tmem + q * 128u + ks * 8u, sw128_desc(v_base + ks * 2048, 16384, 1024),
+                    idesc_o, (issued | ks) != 0);
+          umma_commit(&pv_done[q]);
+        }
+        __syncwarp();
+        ++issued;
+      };
+      // next key tile either query tile uses, and its class nibble (no arrays: an array written
+      // through a pointer lives in local memory, i.e. behind an L2 round trip every tile)
+      auto next_active = [&](int64_t from, uint32_t& nib) {
+        for (int64_t jj = from; jj < j_hi; ++jj) {
+          nib = tile_nib(jj);
+          if (nib != 0) return jj;
+        }
+        nib = 0;
+        return j_hi;
+      };
+      mbar_wait(q_full, 0);
+      uint32_t nib, nib_n;
+      int64_t j = next_active(j_lo, nib);
+      if (j < j_hi) {  // prologue: S of the first active tile
+        mbar_wait(&kv_full[kv_slot(0)], kv_par(0));
+        tc_fence_after();
+        const uint32_t k_base = smem_u32(smem + L::KV_OFF + kv_slot(0) * L::TILE);
+        if (nib & 3u) issue_s(0, k_base);
+        if (nib >> 2) issue_s(1, k_base);
+        if (elect_one()) umma_commit(&kv_empty[kv_slot(0)]);
         __syncwarp();
       }
-      if (elect_one()) umma_commit(&kv_empty[kv_slot(uv)]);
-      __syncwarp();
-      j = jn;
-      cls[0] = cls_n[0];
-      cls[1] = cls_n[1];
+      for (uint32_t t = 0; j < j_hi; ++t) {
+        const int64_t jn = next_active(j + 1, nib_n);
+        const uint32_t uv = 2 * t + 1, uk = 2 * t + 2;
+        if (lane == 0) FWD_PROBE(t, 4);
+        mbar_wait(&kv_full[kv_slot(uv)], kv_par(uv));
+        if (lane == 0) FWD_PROBE(t, 5);
+        tc_fence_after();
+        const uint32_t v_base = smem_u32(smem + L::KV_OFF + kv_slot(uv) * L::TILE);
+        const uint32_t kn_base = smem_u32(smem + L::KV_OFF + kv_slot(uk) * L::TILE);
+        if (nib & 3u) issue_pv(0, v_base, issued0);
+        if (lane == 0) FWD_PROBE(t, 7);
+        if (jn < j_hi) {
+          mbar_wait(&kv_full[kv_slot(uk)], kv_par(uk));
+          tc_fence_after();
+          if (nib_n & 3u) issue_s(0, kn_base);
+        }
+        if (nib >> 2) issue_pv(1, v_base, issued1);
+        if (lane == 0) FWD_PROBE(t, 9);
+        if (jn < j_hi) {
+          if (nib_n >> 2) issue_s(1, kn_base);
+          if (elect_one()) umma_commit(&kv_empty[kv_slot(uk)]);
+          __syncwarp();
+        }
+        if (elect_one()) umma_commit(&kv_empty[kv_slot(uv)]);
+        __syncwarp();
+        j = jn;
+        nib = nib_n;
+      }
     }
-  } else if (warp >= 4) {
-    if constexpr (SPLIT) {
-      fwd_softmax_split<D>(p, smem + L::XCH_OFF, tmem, s_full, p_full, pv_done, m0, j_lo, j_hi, head, tile_cls);
-    } else {
+  } else {
     // ------------------------------------------------ softmax / correction / epilogue
+    setmaxnreg_inc<REGS_SOFTMAX>();
     const int q = (warp - 4) >> 2;  // query tile of this warpgroup
     const uint32_t quad = warp & 3;
     const int row = quad * 32 + lane;
@@ -488,20 +273,16 @@ __global__ void __launch_bounds__(fwd_threads<SPLIT>(), 1)
 
     float m_run = -INFINITY, l_run = 0.f;
     uint32_t t = 0;
-#if BB_FWD_PINGPONG
-    // Exp passes of the two query tiles alternate on MUFU (16 lanes/clk/SM: one 128x128 pass
-    // needs all of it for 1024 cycles).  Left to themselves the two warpgroups drift into phase
-    // and each pass takes twice as long, lengthening the chain softmax(j) -> P.V(j) -> S(j+1).
-    // Only key tiles both query tiles use take turns; order per such tile: tile 0, then 1.
-    uint32_t n_both = 0, k_both = 0;
-    for (int64_t jj = j_lo; jj < j_hi; ++jj) n_both += (tile_nib(jj) & 3u) != 0 && (tile_nib(jj) >> 2) != 0;
-#endif
-    for (int64_t j = j_lo; j < j_hi; ++j) {
-      const int32_t cls = tile_cls(q, j);
-      if (cls == TILE_SKIP) continue;
-#if BB_FWD_PINGPONG
-      const bool both = tile_cls(q ^ 1, j) != TILE_SKIP;
-#endif
+    // The class of the next key tile is read one tile ahead (a shared load behind the MMAs'
+    // operand fetch waits hundreds of cycles; the warp issues in order).
+    int64_t j = j_lo;
+    int32_t cls = j < j_hi ? static_cast<int32_t>((tile_nib(j) >> (2 * q)) & 3u) : TILE_SKIP;
+    for (; j < j_hi; ++j) {
+      const int32_t cls_next = j + 1 < j_hi ? static_cast<int32_t>((tile_nib(j + 1) >> (2 * q)) & 3u) : TILE_SKIP;
+      if (cls == TILE_SKIP) {
+        cls = cls_next;
+        continue;
+      }
       if (row == 0) FWD_PROBE(t, 16 + 8 * q);
       mbar_wait(&s_full[q], t & 1);
       if (row == 0) FWD_PROBE(t, 17 + 8 * q);
@@ -510,40 +291,6 @@ __global__ void __launch_bounds__(fwd_threads<SPLIT>(), 1)
       if (cls == TILE_PARTIAL)
         bits = row_mask_bits(p.layout, p.mask, q_id, row_ok, p.k_device, j * 128, p.n_k, true);
       if (row == 0) FWD_PROBE(t, 22 + 8 * q);
-#if BB_FWD_CHUNKED
-      const uint32_t s_col = tmem + t_lane + q * 128u;
-      float ca[32], cb[32];
-      auto mask_chunk = [&](float(&x)[32], int c0) {
-#pragma unroll
-        for (int c = 0; c < 32; ++c)
-          if (!mask_bit(bits, c0 + c)) x[c] = -INFINITY;
-      };
-      // pass 1: row max, two 32-column loads in flight, 3-input-max tree per chunk
-      float mx8[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        tmem_ld32(s_col + half * 64, ca);
-        tmem_ld32(s_col + half * 64 + 32, cb);
-        tmem_ld_wait();
-        reg_fence(ca);
-        reg_fence(cb);
-        if (cls == TILE_PARTIAL) {
-          mask_chunk(ca, half * 64);
-          mask_chunk(cb, half * 64 + 32);
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          mx8[i] = fmax3(mx8[i], ca[i], ca[i + 8]);
-          mx8[i] = fmax3(mx8[i], ca[i + 16], ca[i + 24]);
-          mx8[i] = fmax3(mx8[i], cb[i], cb[i + 8]);
-          mx8[i] = fmax3(mx8[i], cb[i + 16], cb[i + 24]);
-        }
-      }
-      const float mx = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
-      if (row == 0) FWD_PROBE(t, 23 + 8 * q);
-#else
       float s[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
@@ -566,7 +313,6 @@ __global__ void __launch_bounds__(fwd_threads<SPLIT>(), 1)
 #pragma unroll
       for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(mx8[i], s[120 + i]);
       const float mx = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
-#endif
       const float m_tile = mx * sl2;
       const bool need = m_tile > m_run + RESCALE_THRESHOLD;
       float alpha = 1.f;
@@ -595,51 +341,9 @@ __global__ void __launch_bounds__(fwd_threads<SPLIT>(), 1)
           tmem_st_wait();
         }
       }
-      // P = 2^(S*scale*log2e - m), mostly on MUFU (16 lanes/clk/SM: 1024 clk per 128x128
-      // tile, the same as the tile's two MMAs).  POLY_EVERY moves a share of the columns to a
-      // cubic on the FMA pipe (never for masked tiles, whose -inf scores need MUFU's exact 0).
-      // P is packed to bf16x2 and stored over the S columns it came from, 32 keys at a time.
-      float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#if BB_FWD_CHUNKED
-      // pass 2: reload S chunk by chunk (one load in flight behind the chunk being
-      // exponentiated); P chunk c lands in S columns [c/2, c/2+16), all already read.
-      float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-      const float2 sl2x2 = make_float2(sl2, sl2), negm2 = make_float2(neg_m, neg_m);
-      auto exp_chunk = [&](float(&x)[32], int c0) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float2 y = __ffma2_rn(make_float2(x[2 * i], x[2 * i + 1]), sl2x2, negm2);
-          const float2 e = make_float2(ex2_approx(y.x), ex2_approx(y.y));
-          acc4[i & 3] = __fadd2_rn(acc4[i & 3], e);
-          pk[i] = pack_bf16(e.x, e.y);
-        }
-        tmem_st16(s_col + c0 / 2, pk);
-      };
-      tmem_ld32(s_col, ca);
-      tmem_ld32(s_col + 32, cb);
-      tmem_ld_wait();
-      reg_fence(ca);
-      reg_fence(cb);
-      if (cls == TILE_PARTIAL) {
-        mask_chunk(ca, 0);
-        mask_chunk(cb, 32);
-      }
-      exp_chunk(ca, 0);
-      tmem_ld32(s_col + 64, ca);
-      exp_chunk(cb, 32);
-      tmem_ld_wait();
-      reg_fence(ca);
-      tmem_ld32(s_col + 96, cb);
-      if (cls == TILE_PARTIAL) mask_chunk(ca, 64);
-      exp_chunk(ca, 64);
-      tmem_ld_wait();
-      reg_fence(cb);
-      if (cls == TILE_PARTIAL) mask_chunk(cb, 96);
-      exp_chunk(cb, 96);
-#elif BB_FWD_X2
-      // packed fp32x2 arithmetic (FFMA2 for the scale, FADD2 for the row sums): half the FP32
-      // issue slots of the scalar form; POLY_EVERY (in pairs) moves a share to ex2_poly2.
+      // P = 2^(S*scale*log2e - m) with packed fp32x2 arithmetic (FFMA2 for the scale, FADD2 for
+      // the row sums), packed to bf16x2 and stored over the S columns it came from, 32 keys at a
+      // time.  Masked tiles stay on MUFU (its ex2(-inf) = 0 is exact).
       float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       const float2 sl2x2 = make_float2(sl2, sl2), negm2 = make_float2(neg_m, neg_m);
       auto exp_pass = [&](auto masked_tag) {
@@ -648,75 +352,22 @@ __global__ void __launch_bounds__(fwd_threads<SPLIT>(), 1)
         for (int c = 0; c < 128; c += 32) {
           uint32_t pk[16];
 #pragma unroll
-          for (int h = 0; h < 32; h += 8) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float2 x = __ffma2_rn(make_float2(s[c + h + 2 * i], s[c + h + 2 * i + 1]), sl2x2, negm2);
-              const float2 e = (!MASKED && (i % POLY_EVERY) == POLY_EVERY - 1)
-                                   ? ex2_poly2(x)
-                                   : make_float2(ex2_approx(x.x), ex2_approx(x.y));
-              acc4[i] = __fadd2_rn(acc4[i], e);
-              pk[h / 2 + i] = pack_bf16(e.x, e.y);
-            }
+          for (int i = 0; i < 16; ++i) {
+            const float2 x = __ffma2_rn(make_float2(s[c + 2 * i], s[c + 2 * i + 1]), sl2x2, negm2);
+            const float2 e = (!MASKED && BB_FWD_POLY > 0 && (i % (BB_FWD_POLY > 0 ? BB_FWD_POLY : 1)) == 0)
+                                 ? ex2_poly2(x)
+                                 : make_float2(ex2_approx(x.x), ex2_approx(x.y));
+            acc4[i & 3] = __fadd2_rn(acc4[i & 3], e);
+            pk[i] = pack_bf16(e.x, e.y);
           }
           tmem_st16(tmem + t_lane + q * 128u + c / 2, pk);
         }
       };
-#else
-      auto exp_pass = [&](auto masked_tag) {
-        constexpr bool MASKED = decltype(masked_tag)::value;
-#pragma unroll
-        for (int c = 0; c < 128; c += 32) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int h = 0; h < 32; h += 8) {
-            float e[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float x = fmaf(s[c + h + i], sl2, neg_m);
-              e[i] = (!MASKED && (i % POLY_EVERY) == POLY_EVERY - 1) ? ex2_poly(x) : ex2_approx(x);
-              acc8[i] += e[i];
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#if BB_PACK_INT
-              pk[h / 2 + i] = pack_bf16_int(e[2 * i], e[2 * i + 1]);
-#else
-              pk[h / 2 + i] = pack_bf16(e[2 * i], e[2 * i + 1]);
-#endif
-          }
-          tmem_st16(tmem + t_lane + q * 128u + c / 2, pk);
-        }
-      };
-#endif
-#if BB_FWD_PINGPONG
-      // tile 0 waits for tile 1's pass of the previous shared key tile; tile 1 for tile 0's
-      // pass of this one (bar.sync by the waiting warpgroup + bar.arrive by the other = 256)
-      if (both && (q == 1 || k_both > 0)) named_bar_sync(1 + q, 256);
-#endif
-#if !BB_FWD_CHUNKED
       if (cls == TILE_PARTIAL)
         exp_pass(std::true_type{});
       else
         exp_pass(std::false_type{});
-#endif
-#if BB_FWD_PINGPONG
-      if (both) {
-        if (q == 0 || k_both + 1 < n_both) named_bar_arrive(2 - q, 256);
-        ++k_both;
-      }
-#endif
-#if BB_FWD_X2 || BB_FWD_CHUNKED
-      acc8[0] = acc4[0].x;
-      acc8[1] = acc4[0].y;
-      acc8[2] = acc4[1].x;
-      acc8[3] = acc4[1].y;
-      acc8[4] = acc4[2].x;
-      acc8[5] = acc4[2].y;
-      acc8[6] = acc4[3].x;
-      acc8[7] = acc4[3].y;
-#endif
-      l_run += ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
+      l_run += ((acc4[0].x + acc4[0].y) + (acc4[1].x + acc4[1].y)) + ((acc4[2].x + acc4[2].y) + (acc4[3].x + acc4[3].y));
       if (row == 0) FWD_PROBE(t, 20 + 8 * q);
       tmem_st_wait();
       if (row == 0) FWD_PROBE(t, 21 + 8 * q);
@@ -724,6 +375,7 @@ __global__ void __launch_bounds__(fwd_threads<SPLIT>(), 1)
       mbar_arrive(&p_full[q]);
       if (row == 0) FWD_PROBE(t, 19 + 8 * q);
       ++t;
+      cls = cls_next;
     }
 
     if (t > 0) {
@@ -771,7 +423,6 @@ __global__ void __launch_bounds__(fwd_threads<SPLIT>(), 1)
         }
       }
     }
-    }  // !SPLIT
   }
 
   tc_fence_before();
@@ -803,9 +454,8 @@ int launch_fwd_d(const bb_attn_fwd_args& a, cudaStream_t st) {
   p.mask = make_maskd(a.mask);
   p.q_pairs = static_cast<int32_t>((a.n_q + 255) / 256);
   p.probe = debug_probe_buffer();
-  constexpr bool SPLIT = BB_FWD_SPLIT != 0;
-  using L = FwdSmem<D, SPLIT>;
-  auto kern = attn_fwd_kernel<D, SPLIT>;
+  using L = FwdSmem<D>;
+  auto kern = attn_fwd_kernel<D>;
   static uint64_t attr_done = 0;  // per device: the attribute is per-context
   int dev = 0;
   cudaGetDevice(&dev);
@@ -816,7 +466,7 @@ int launch_fwd_d(const bb_attn_fwd_args& a, cudaStream_t st) {
     attr_done |= uint64_t(1) << dev;
   }
   dim3 grid(p.q_pairs, a.hq);
-  kern<<<grid, fwd_threads<SPLIT>(), L::BYTES, st>>>(tq, tk, tv, p);
+  kern<<<grid, FWD_THREADS, L::BYTES, st>>>(tq, tk, tv, p);
   return check_launch("attn_fwd_kernel");
 }
 
