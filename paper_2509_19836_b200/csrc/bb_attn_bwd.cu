@@ -87,10 +87,16 @@ struct BwdParams {
   long long* probe;  // diagnostics: per-phase clock64() of CTA (0,0), see bb_debug_probe
 };
 
+#ifndef BB_WITH_PROBES  // per-phase clock64 probes: diagnostic builds only (tools/variant.py probes BB_WITH_PROBES)
+#define BB_PROBE(slot) \
+  do {                 \
+  } while (0)
+#else
 #define BB_PROBE(slot)                                                                 \
   do {                                                                                 \
     if (p.probe && blockIdx.x == 0 && blockIdx.y == 0 && it < 16) p.probe[it * 32 + (slot)] = clock64(); \
   } while (0)
+#endif
 
 __device__ __forceinline__ int32_t bwd_class(const BwdParams& p, int64_t qt, int64_t c0) {
   const int64_t r0 = qt * 128, r1 = min(r0 + 128, p.n_q);

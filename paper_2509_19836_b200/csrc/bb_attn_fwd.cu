@@ -69,10 +69,16 @@ struct FwdParams {
   long long* probe;  // diagnostics (BB_PROBE=1): clock64() per phase of CTA (0,0)
 };
 
+#ifndef BB_WITH_PROBES  // per-phase clock64 probes: diagnostic builds only (tools/variant.py probes BB_WITH_PROBES)
+#define FWD_PROBE(idx, slot) \
+  do {                 \
+  } while (0)
+#else
 #define FWD_PROBE(idx, slot)                                                                         \
   do {                                                                                               \
     if (p.probe && blockIdx.x == 0 && blockIdx.y == 0 && (idx) < 16) p.probe[512 + (idx) * 32 + (slot)] = clock64(); \
   } while (0)
+#endif
 
 __device__ __forceinline__ int32_t fwd_class(const FwdParams& p, int q, int64_t m0, int64_t j) {
   const int64_t r0 = m0 + 128 * q;

@@ -5,6 +5,8 @@ import runpy
 import sys
 
 os.environ["BB_PROBE"] = "1"
+# the product library compiles the probes out: build `python tools/variant.py probes BB_WITH_PROBES`
+os.environ.setdefault("BB_LIB_PATH", "tools/exp_lib/probes/libburst_b200.so")
 import numpy as np
 
 from paper_2509_19836_b200 import _native as N

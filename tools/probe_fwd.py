@@ -1,6 +1,8 @@
 """Per-phase clock64 timeline of one forward CTA (BB_PROBE=1)."""
 import os, sys, runpy
 os.environ["BB_PROBE"] = "1"
+# the product library compiles the probes out: build `python tools/variant.py probes BB_WITH_PROBES`
+os.environ.setdefault("BB_LIB_PATH", "tools/exp_lib/probes/libburst_b200.so")
 import numpy as np
 from paper_2509_19836_b200 import _native as N
 sys.argv = ["perf_attn.py", "--n", "32768", "--heads", "8", "--iters", "1", "--mask", "full"] + sys.argv[1:]
