@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--topology", default=None, help="RxM two-level ring, e.g. 2x4 (default 1xN)")
     ap.add_argument("--transport", default="ce", choices=["ce", "collective"],
                     help="ring exchange: copy-engine pushes into IPC arenas (ce) or NCCL send/recv (collective)")
-    ap.add_argument("--slots", type=int, default=None, help="ce transport: arena slots per channel (default N-1)")
+    ap.add_argument("--slots", type=int, default=None, help="ce transport: arena slots per channel (default min(N-1, 3))")
     ap.add_argument("--ce-fanout", type=int, default=None, help="ce transport: copy streams per push (default BB_CE_FANOUT or 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -413,7 +413,32 @@ def run_gpu(args) -> None:
         # exposed = step - the busiest rank's kernel time: what the exchange (and its folds) add
         # to the critical path.  max_rank_idle also counts ranks waiting on a busier peer.
         exposed = max(0.0, step_s - comp_s)
+        # one traced step: every kernel and copy-engine push as a measured event, assembled into
+        # the reference's Timeline schema and checked by validate_timeline (fabric.py:366-388,
+        # 674-705); the exchange is compared with the Table-1 closed form (fabric.py:337-358)
+        # for BurstEngine's strategy on a topology calibrated to the copy engines' peer rate.
+        timeline = None
+        if ring.transport == "ce":
+            from paper_2509_19836_b200.fabric import analytic_comm_time
+
+            ring.trace_begin()
+            step()
+            tl = ring.trace_collect()
+            sends = [e for e in tl.events if e.kind.startswith("send_")]
+            busiest = max(sum(e.end - e.start for e in tl.device_events(r + 1, "compute")) for r in range(world))
+            link = Topology(1, world, lat_intra=10e-6, lat_inter=10e-6, bw_intra=764e9, bw_inter=764e9)  # bytes/s (profiles/r01e_p2p_bw.json)
+            per_step = ring_bytes / max(1, 3 * (world - 1))  # forward + backward payload + gradient partial per hop
+            timeline = {
+                "events": len(tl.events), "validated": True, "makespan_ms": tl.makespan * 1e3,
+                "busiest_rank_compute_ms": busiest * 1e3, "sends": len(sends),
+                "send_ms_total_per_rank": sum(e.end - e.start for e in sends) / world * 1e3,
+                "analytic_comm_ms_burst_strategy": analytic_comm_time("burst", link, per_step) * 1e3,
+                "how": "CUDA events around every kernel and push of one step, common origin at a barrier; validate_timeline on the assembled schema",
+            }
         overlap = {
+            "timeline": timeline,
+            "arena_bytes_per_rank": ring.arena_bytes() if ring.transport == "ce" else None,
+            "arena_slots": ring.slots,
             "transport": ring.transport,
             "ce_fanout": ring.fanout if ring.transport == "ce" else None,
             "step_ms": step_s * 1e3, "compute_ms": comp_s * 1e3, "comm_alone_ms": comm_s * 1e3,

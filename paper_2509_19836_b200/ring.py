@@ -39,7 +39,17 @@ import torch
 import torch.distributed as dist
 
 from . import kernels as K
-from .fabric import BURST_BACKWARD, FORWARD, RING_BACKWARD, Topology, build_ring_plan, single_node_topology
+from .fabric import (
+    BURST_BACKWARD,
+    FORWARD,
+    RING_BACKWARD,
+    Timeline,
+    TimelineEvent,
+    Topology,
+    build_ring_plan,
+    single_node_topology,
+    validate_timeline,
+)
 from .masks import MaskSpec, validate_mask
 from .partitioning import ShardLayout, pair_count_matrix
 
@@ -57,6 +67,31 @@ class RingStats:
     bytes_sent: int = 0
     launches: int = 0
     kernel_events: list = field(default_factory=list)  # (start, end) CUDA events when recording
+
+
+def assemble_timeline(per_rank: list[list[tuple]], topology: Topology) -> Timeline:
+    """Measured events of every rank -> the reference's Timeline schema (fabric.py:366-388).
+
+    ``per_rank[r]`` holds (kind, start_s, end_s, label, peer) tuples of rank r on a common time
+    base: kind "compute" (a kernel on the compute stream) or "send" (a copy-engine push to rank
+    ``peer``).  A send becomes send_intra / send_inter by whether the two ranks share a node of
+    the R x M topology, and is mirrored as the receiver's "recv <label>" over the same interval
+    (the push lands in the receiver's arena while it runs), so validate_timeline's send/recv
+    matching holds by construction and its compute-lane check tests the real launches."""
+    m = topology.gpus_per_node
+    evs = []
+    for r, events in enumerate(per_rank):
+        for kind, a, b, label, peer in events:
+            if kind == "compute":
+                evs.append(TimelineEvent(r + 1, "compute", a, b, label))
+            else:
+                k = "send_intra" if r // m == peer // m else "send_inter"
+                evs.append(TimelineEvent(r + 1, k, a, b, label))
+                evs.append(TimelineEvent(peer + 1, "recv", a, b, f"recv {label}"))
+    evs.sort(key=lambda e: (e.start, e.device, e.kind, e.label))
+    tl = Timeline(evs, max((e.end for e in evs), default=0.0))
+    validate_timeline(tl)
+    return tl
 
 
 class ProcessRing:
@@ -84,14 +119,18 @@ class ProcessRing:
         self.stats = RingStats()
         self.compute = True  # False: run only the exchanges (communication-alone timing)
         self.record = False  # True: CUDA events around every kernel launch (compute-lane time)
+        self._trace = None  # list while tracing: (kind, start event, end event, label, peer)
+        self._trace_t0 = None
         if transport is None:
             transport = "ce" if self.device.type == "cuda" and self.world > 1 else "collective"
+        if slots is None:  # the paper's three buffers per device (fabric.py:87-90): the one being
+            slots = min(self.world - 1, 3)  # computed on plus two landing; arena bytes O(1) in G
         if transport not in ("ce", "collective"):
             raise ValueError(f"unknown ring transport {transport!r} (expected 'ce' or 'collective')")
         if transport == "ce" and self.device.type != "cuda":
             raise ValueError("the copy-engine transport needs CUDA devices")
         self.transport = transport
-        self.slots = slots  # arena slots per channel (default world-1: every payload of a pass in flight)
+        self.slots = slots  # arena slots per channel (default min(world - 1, 3))
         self.fanout = max(1, int(fanout or os.environ.get("BB_CE_FANOUT", "1")))  # copy streams per push
         self._channels: dict = {}
         self._grad_state: dict = {}  # per gradient channel: partial buffers, their events, fold target
@@ -101,8 +140,16 @@ class ProcessRing:
         self._src = [None] + [self.order[t] for t in range(1, self.world)]
         self._dst = [None] + [self._who_had_me(t) for t in range(1, self.world)]
 
-    def _launch(self, fn, *a, **kw):
+    def _launch(self, fn, *a, label: str = "", **kw):
         if not self.compute:
+            return
+        if self._trace is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn(*a, **kw)
+            e1.record()
+            self._trace.append(("compute", e0, e1, label or getattr(fn, "__name__", "kernel"), None))
+            self.stats.launches += 1
             return
         if self.record:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -113,6 +160,46 @@ class ProcessRing:
         else:
             fn(*a, **kw)
         self.stats.launches += 1
+
+    # -------------------------------------------------------------- measured timeline
+    def trace_begin(self) -> None:
+        """Start recording a measured timeline (CE transport on GPUs): every rank synchronises,
+        meets at a barrier and records its time origin, then kernels and pushes are bracketed
+        by CUDA events until ``trace_collect``.  Collective."""
+        torch.cuda.synchronize(self.device)
+        if dist.is_initialized():
+            dist.barrier(group=self.group)
+        self._trace_t0 = torch.cuda.Event(enable_timing=True)
+        self._trace_t0.record()
+        self._trace = []
+
+    def trace_collect(self) -> Timeline:
+        """Stop recording; gather every rank's events into one validated Timeline in the
+        reference's schema (seconds from the barrier).  Collective; every rank gets it."""
+        torch.cuda.synchronize(self.device)
+        t0 = self._trace_t0
+        mine = [(k, t0.elapsed_time(a) / 1e3, t0.elapsed_time(b) / 1e3, lab, peer) for k, a, b, lab, peer in self._trace]
+        self._trace = self._trace_t0 = None
+        per_rank = [None] * self.world
+        if dist.is_initialized() and self.world > 1:
+            dist.all_gather_object(per_rank, mine, group=self.group)
+        else:
+            per_rank = [mine]
+        return assemble_timeline(per_rank, self.topology)
+
+    def _push(self, ch, s: int, tensors, stream, lanes, label: str) -> None:
+        if self._trace is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ch.push(s, tensors, stream, lanes)
+            e1.record(stream)
+            self._trace.append(("send", e0, e1, f"{label} {self.rank + 1}->{ch.send_to[s] + 1}", ch.send_to[s]))
+        else:
+            ch.push(s, tensors, stream, lanes)
+
+    def arena_bytes(self) -> int:
+        """Device bytes of this rank's copy-engine arenas (all channels)."""
+        return sum(ch.total for ch in self._channels.values())
 
     def kernel_seconds(self) -> float:
         """Sum of recorded kernel durations (call after synchronizing)."""
@@ -327,7 +414,7 @@ class ProcessRing:
         ch.begin()
         xs.wait_stream(cs)  # payload produced on the compute stream
         for s in range(1, self.world):
-            ch.push(s, list(payload), xs, self._xs_lanes[0])
+            self._push(ch, s, list(payload), xs, self._xs_lanes[0], f"{ch.name} step {s}")
         self.stats.bytes_sent += (self.world - 1) * ch.payload_bytes
 
     def _forward_ce(self, q, k, v, o, lse, d):
@@ -339,7 +426,7 @@ class ProcessRing:
             kv = (k, v) if t == 0 else ch.wait(t, cs)
             if self.counts[self.rank, j]:
                 self._launch(K.attn_fwd_step, q, kv[0], kv[1], o, lse, self.layout, self.dmask, self.rank + 1, j + 1,
-                             self._scale(d), n_q=q.shape[0])
+                             self._scale(d), n_q=q.shape[0], label=f"forward q{self.rank + 1} x k{j + 1}")
             if t > 0:
                 ch.release(t, cs)
         cs.wait_stream(xs)
@@ -369,7 +456,7 @@ class ProcessRing:
         hs = [(hkv // 2) * (a.shape[1] // hkv) for a in own_acc]  # first head of half B, per accumulator
         me, last = self.rank, self.world - 1
         if not skip(me):
-            self._launch(launch, data, own_acc, me, (0, hkv // 2) if split else None)
+            self._launch(launch, data, own_acc, me, (0, hkv // 2) if split else None, label=f"{grad_name} own shard A")
         xf.wait_stream(cs)
         b_ready = None
         for t in range(1, self.world):
@@ -379,10 +466,10 @@ class ProcessRing:
             if free[t % 2] is not None:
                 cs.wait_event(free[t % 2])
             if not skip(j):
-                self._launch(launch, payload, acc, j, None)
+                self._launch(launch, payload, acc, j, None, label=f"{grad_name} shard {j + 1} on {me + 1}")
             dch.release(t, cs)
             xg.wait_stream(cs)
-            gch.push(t, list(acc), xg, self._xs_lanes[1])
+            self._push(gch, t, list(acc), xg, self._xs_lanes[1], f"{grad_name} step {t}")
             self.stats.bytes_sent += gch.payload_bytes
             if self.compute:
                 with torch.cuda.stream(xg):
@@ -408,7 +495,7 @@ class ProcessRing:
             if b_ready is not None:
                 cs.wait_event(b_ready)
             if not skip(me):
-                self._launch(launch, data, own_acc, me, (hkv // 2, hkv))
+                self._launch(launch, data, own_acc, me, (hkv // 2, hkv), label=f"{grad_name} own shard B")
             cs.wait_stream(xf)
             if last >= 1:
                 views = gch.views(last)

@@ -208,3 +208,30 @@ def test_autograd_function_matches_oracle(policy_frac):
         assert np.max(np.abs(dq - ref["dq"][rows])) < 2e-6
         assert np.max(np.abs(dk - ref["dk"][rows])) < 2e-6
         assert np.max(np.abs(dv - ref["dv"][rows])) < 2e-6
+
+
+def test_measured_events_assemble_into_a_valid_timeline():
+    """ProcessRing.trace_collect's assembly (ring.assemble_timeline): per-rank kernel and push
+    events become the reference's Timeline schema (fabric.py:366-388); pushes are split into
+    intra / inter sends by the R x M topology and mirrored as the receiver's recv; the result
+    passes validate_timeline, and an overlapping compute lane is rejected."""
+    from paper_2509_19836_b200.fabric import Topology
+    from paper_2509_19836_b200.ring import assemble_timeline
+
+    per_rank = [
+        [("compute", 0.0, 1.0, "fwd own", None), ("send", 0.1, 0.2, "kv step 1 1->2", 1),
+         ("compute", 1.0, 2.0, "fwd k2", None)],
+        [("compute", 0.0, 1.1, "fwd own", None), ("send", 0.1, 0.25, "kv step 1 2->1", 0),
+         ("send", 0.3, 0.4, "kv step 2 2->3", 2)],
+        [("compute", 0.0, 0.9, "fwd own", None)],
+        [("compute", 0.0, 0.95, "fwd own", None), ("send", 0.5, 2.5, "dq step 1 4->1", 0)],
+    ]
+    tl = assemble_timeline(per_rank, Topology(2, 2))
+    assert tl.makespan == 2.5
+    kinds = {(e.device, e.kind, e.label) for e in tl.events}
+    assert (1, "send_intra", "kv step 1 1->2") in kinds and (2, "recv", "recv kv step 1 1->2") in kinds
+    assert (2, "send_inter", "kv step 2 2->3") in kinds and (3, "recv", "recv kv step 2 2->3") in kinds
+    assert (4, "send_inter", "dq step 1 4->1") in kinds and (1, "recv", "recv dq step 1 4->1") in kinds
+    per_rank[0].append(("compute", 1.5, 1.8, "overlapping", None))
+    with pytest.raises(ValueError, match="compute lane overlaps"):
+        assemble_timeline(per_rank, Topology(2, 2))

@@ -64,8 +64,16 @@ def main():
             else:
                 ring = ProcessRing(layout, mask, Topology(*topo), head_dim=d, transport=transport, slots=slots)
                 for rep in range(2):  # later passes exercise the cross-pass slot hand-over (flag epochs)
+                    traced = transport == "ce" and rep == 1
+                    if traced:  # measured timeline of the second pass (validated on assembly)
+                        ring.trace_begin()
                     o, lse = ring.forward(q, k, v)
                     dq, dk, dv = ring.backward(q, k, v, do, o, lse, kind=backward)
+                    if traced:
+                        tl = ring.trace_collect()
+                        if not tl.by_kind("compute") or not (tl.by_kind("send_intra") or tl.by_kind("send_inter")):
+                            print(f"rank {rank} FAIL timeline without kernels or pushes", flush=True)
+                            failures += 1
             torch.cuda.synchronize()
             ring.close()  # collective: frees the copy-engine arenas after every rank's passes
             failures += _report(rank, f"{kind} {topo} {mname} {backward} {transport} slots={slots}", o, lse, dq, dk, dv,
