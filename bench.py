@@ -524,6 +524,12 @@ def run_gpu(args) -> None:
         }
 
     lm = None if args.no_lmhead else run_lmhead(args, dev, world)
+    e2e_api = None
+    if world == 1 and not args.no_e2e:
+        host = [x.float().cpu().numpy() for x in (q, k, v, do)]
+        del q, k, v, do, o, lse, dq, dk, dv
+        torch.cuda.empty_cache()
+        e2e_api = run_dropin_e2e(args, layout, mask, host, flops_step)
 
     if rank != 0:
         if world > 1:
@@ -576,6 +582,7 @@ def run_gpu(args) -> None:
         "ring_bytes_sent_per_step_rank0": ring_bytes,
         "ring_overlap": overlap,
         "lmhead": lm,
+        "e2e_dropin_api": e2e_api,
     }
     if lm is not None:
         lm["roofline"]["peak"] = peak
@@ -585,6 +592,44 @@ def run_gpu(args) -> None:
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_dropin_e2e(args, layout, mask, host, flops_step: float, steps: int = 2) -> dict:
+    """The burstsim call sequence a drop-in caller makes (distributed.py:104-130, 151-303):
+    NumPy arrays in -> make_device_states -> distributed_forward -> burst_backward(shard_rows(dO))
+    -> backward_grads -> float64 NumPy gradients out, every byte of it inside the timed region
+    (pageable host memory, as a NumPy caller has it).  Wall clock around synchronised steps."""
+    import torch
+
+    import paper_2509_19836_b200 as bb
+
+    q, k, v, do = host
+
+    def once():
+        st = bb.make_device_states(layout, q, k, v)
+        bb.distributed_forward(st, layout, mask)
+        bb.burst_backward(st, bb.shard_rows(layout, do), layout, mask)
+        g = bb.backward_grads(st)
+        return g
+
+    once()  # warm-up (allocations, descriptors)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        g = once()
+    torch.cuda.synchronize()
+    t = (time.perf_counter() - t0) / steps
+    return {
+        "value": flops_step / t / 1e12,
+        "unit": "TFLOPS",
+        "ms_per_step": t * 1e3,
+        "steps": steps,
+        "h2d_bytes_per_step": sum(x.nbytes for x in host),
+        "d2h_bytes_per_step": sum(x.size * 4 for x in (g[0].dq, g[0].dk, g[0].dv)),
+        "output_dtype": str(g[0].dq.dtype),
+        "how": "NumPy float32 [N, H, d] in, float64 NumPy dQ/dK/dV out through make_device_states, distributed_forward, "
+        "burst_backward, backward_grads; host wall clock, pageable memory, conversions included",
+    }
 
 
 def run_lmhead(args, dev, world: int) -> dict:

@@ -95,7 +95,7 @@ class DeviceState:
         t = getattr(self, name)
         if t is None:
             raise RuntimeError(f"{name} has not been computed")
-        a = t.detach().float().cpu().numpy().astype(np.float64)
+        a = t.detach().float().cpu().double().numpy()  # torch's multi-threaded host cast, not NumPy's single-threaded one
         if name in ("lse", "d_vec"):
             return a[0] if self.single_head else a
         a = a[..., : self.head_dim]
