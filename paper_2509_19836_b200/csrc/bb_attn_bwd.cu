@@ -558,6 +558,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     constexpr int CHUNKS = D / 32;
     // (16-column chunks through 8 KB SWIZZLE_64B slots measured 10 % slower: twice the
     // barriers per tile, and half-line reduce rows.
+    // (An FMA-pipe exp2 share in the P pass, 1/8 .. 1/2 of the pairs: no change, 989-996 vs
+    // 1000 TF/s -- the P pass is not MUFU-bound here.)
     // Coalesced red.global.add.v4.f32 (4 rows x 128 B per warp instruction, read back from the
     // staging slot) for every other chunk, TMA reduce for the rest: 903 vs 1014 TF/s.
     // red.global.add.v4.f32 from registers for half the columns measured 20 % slower overall:
