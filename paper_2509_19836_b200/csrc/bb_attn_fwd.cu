@@ -38,7 +38,9 @@ constexpr int MAX_KT = 4096;  // key tiles per shard the class table holds (n_k 
 constexpr int KV_SLOTS = 5;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units: P may reach 2^8 before O is rescaled
 constexpr uint32_t REGS_CTRL = 64, REGS_SOFTMAX = 216;
-static_assert(REGS_CTRL * 128 + REGS_SOFTMAX * 256 <= 65536, "register budget");
+// setmaxnreg.inc blocks until the CTA's pool has the registers: the pool is what the launch
+// allocated (168 per thread at 384 threads), not the 64K register file.
+static_assert(REGS_CTRL * 128 + REGS_SOFTMAX * 256 <= 168 * FWD_THREADS, "register budget");
 #ifndef BB_FWD_POLY
 // Every BB_FWD_POLY-th exponential pair of an unmasked tile goes to a cubic on the FMA pipe
 // (ex2_poly2) instead of MUFU (16 lanes/clk/SM: a 128x128 tile's exps need as many cycles as
