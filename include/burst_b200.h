@@ -100,6 +100,11 @@ typedef struct bb_attn_fwd_args {
   int32_t k_device;
   bb_layout layout;
   bb_mask mask;
+  /* Optional (NULL = off): also store bf16(O) [n_q, hq, head_dim] after this step's merge,
+   * for every row < n_q (rows this step does not touch are copied from O).  Passed on the
+   * last ring step, it fuses the cast the output projection's bf16 GEMM needs
+   * (bb_gemm_bf16_rows, AttentionParams.w_attn, oracle.py:29-44). */
+  void* o_bf16;
 } bb_attn_fwd_args;
 
 /* One backward ring step (K/V-stationary kernel).  Accumulates, in f32:

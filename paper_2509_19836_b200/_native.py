@@ -89,6 +89,7 @@ class BbAttnFwdArgs(C.Structure):
         ("k_device", C.c_int32),
         ("layout", BbLayout),
         ("mask", BbMask),
+        ("o_bf16", C.c_void_p),
     ]
 
 

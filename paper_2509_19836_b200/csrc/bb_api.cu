@@ -171,6 +171,8 @@ int bb_attn_fwd_step(const bb_attn_fwd_args* a, void* stream) {
   if (int rc = validate_ring_step(a->layout, a->mask, a->n_q, a->n_k, a->hq, a->hkv, a->head_dim, a->q_device,
                                   a->k_device, "bb_attn_fwd_step"))
     return rc;
+  if (a->o_bf16 && (reinterpret_cast<uintptr_t>(a->o_bf16) & 15))
+    return set_error(BB_ERR_INVALID, "bb_attn_fwd_step: o_bf16 must be 16-byte aligned");
   return launch_attn_fwd(*a, static_cast<cudaStream_t>(stream));
 }
 

@@ -68,6 +68,7 @@ struct FwdParams {
   LayoutD layout;
   MaskD mask;
   int32_t q_pairs;  // number of 256-row query blocks
+  uint2* o16;       // optional bf16 copy of O after the merge (4 columns per uint2)
   long long* probe;  // diagnostics (BB_PROBE=1): clock64() per phase of CTA (0,0)
 };
 
@@ -386,13 +387,17 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       cls = cls_next;
     }
 
+    float* o_row = p.o + (qrow * p.hq + head) * static_cast<int64_t>(D);
+    uint2* o16_row = (p.o16 && row_ok) ? p.o16 + (qrow * p.hq + head) * static_cast<int64_t>(D / 4) : nullptr;
+    bool written = false;
     if (t > 0) {
       mbar_wait(&pv_done[q], (t - 1) & 1);
       tc_fence_after();
       // lse_step in natural log: sum exp(S) = 2^m_run * l_run.
       const float lse_step = (l_run > 0.f) ? (m_run * 0.69314718055994531f + logf(l_run)) : -INFINITY;
       float w_step = 0.f, w_old = 0.f, lse_new = -INFINITY;
-      bool write = row_ok && lse_step != -INFINITY;
+      const bool write = row_ok && lse_step != -INFINITY;
+      written = write;
       float* lse_ptr = p.lse + static_cast<int64_t>(head) * p.n_q + qrow;
       if (write) {
         const float lse_prev = *lse_ptr;
@@ -407,7 +412,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         }
         *lse_ptr = lse_new;
       }
-      float* o_row = p.o + (qrow * p.hq + head) * static_cast<int64_t>(D);
 #pragma unroll 1
       for (int c = 0; c < D / 32; ++c) {
         float o[32];
@@ -427,8 +431,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
               r.w += w_old * prev.w;
             }
             dst[i] = r;
+            if (o16_row) o16_row[c * 8 + i] = make_uint2(pack_bf16(r.x, r.y), pack_bf16(r.z, r.w));
           }
         }
+      }
+    }
+    // Rows this step leaves untouched still need their bf16 copy (the running O as it is).
+    if (o16_row && !written) {
+      const float4* src = reinterpret_cast<const float4*>(o_row);
+#pragma unroll 4
+      for (int i = 0; i < D / 4; ++i) {
+        const float4 r = src[i];
+        o16_row[i] = make_uint2(pack_bf16(r.x, r.y), pack_bf16(r.z, r.w));
       }
     }
   }
@@ -462,6 +476,7 @@ int launch_fwd_d(const bb_attn_fwd_args& a, cudaStream_t st) {
   p.mask = make_maskd(a.mask);
   p.q_pairs = static_cast<int32_t>((a.n_q + 255) / 256);
   p.probe = debug_probe_buffer();
+  p.o16 = static_cast<uint2*>(a.o_bf16);
   using L = FwdSmem<D>;
   auto kern = attn_fwd_kernel<D>;
   static uint64_t attr_done = 0;  // per device: the attribute is per-context

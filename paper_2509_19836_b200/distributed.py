@@ -82,6 +82,7 @@ class DeviceState:
     dq: torch.Tensor | None = None
     dk: torch.Tensor | None = None
     dv: torch.Tensor | None = None
+    o16: torch.Tensor | None = None  # bf16 copy of O from the last forward step (emit_o_bf16)
     head_dim: int = 0  # unpadded d (softmax scale 1/sqrt(d))
     single_head: bool = False  # caller passed 2-D [N, d] arrays
     token_rows: torch.Tensor | None = field(default=None, repr=False)  # 0-based global rows (int64, device)
@@ -316,8 +317,12 @@ def distributed_forward(
     visit_order: list[list[int]] | None = None,
     schedule: OverlapSchedule | None = None,
     _exec: _Executor | None = None,
+    emit_o_bf16: bool = False,
 ) -> MessageLog:
-    """Ring forward (Alg. 3): fills each state's (o, lse) in place (distributed.py:151-195)."""
+    """Ring forward (Alg. 3): fills each state's (o, lse) in place (distributed.py:151-195).
+
+    ``emit_o_bf16``: each device's last launched step also stores bf16(O) into ``state.o16``
+    (the cast the output projection's GEMM needs, fused into the merge epilogue)."""
     _check_states(states, layout)
     validate_mask(mask, layout.seq_len)
     plan = _plan_for(layout, topology)
@@ -329,6 +334,9 @@ def distributed_forward(
         st.o = torch.zeros(st.q.shape, dtype=torch.float32, device=st.device)
         st.lse = torch.full((st.q.shape[1], st.q.shape[0]), float("-inf"), device=st.device)
     masks = {st.device: K.device_mask(mask, st.device) for st in states}
+    last = [max((t for t in range(g) if counts[i, order[i][t]]), default=-1) for i in range(g)]
+    for i, st in enumerate(states):
+        st.o16 = torch.empty(st.q.shape, dtype=torch.bfloat16, device=st.device) if emit_o_bf16 else None
     for t in range(g):
         for i, st in enumerate(states):
             j = order[i][t]
@@ -336,11 +344,12 @@ def distributed_forward(
                 continue  # compute skipped; the ring step itself is still accounted (:178-179)
             src = states[j]
             k_j, v_j = ex.fetch((src.k, src.v), st.device, j, i, f"fwd step {t + 1} kv {j + 1}->{i + 1}")
+            o16 = st.o16 if t == last[i] else None
             ex.compute(
                 i,
                 f"fwd step {t + 1} shard {j + 1}",
-                lambda st=st, k_j=k_j, v_j=v_j, j=j: K.attn_fwd_step(
-                    st.q, k_j, v_j, st.o, st.lse, layout, masks[st.device], st.index, j + 1, _scale(st)
+                lambda st=st, k_j=k_j, v_j=v_j, j=j, o16=o16: K.attn_fwd_step(
+                    st.q, k_j, v_j, st.o, st.lse, layout, masks[st.device], st.index, j + 1, _scale(st), o_bf16=o16
                 ),
             )
     for st in states:  # a globally fully-masked row is an error (distributed.py:189-194)

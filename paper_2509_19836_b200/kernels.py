@@ -117,18 +117,24 @@ def attn_fwd_step(
     k_device: int,
     softmax_scale: float,
     n_q: int | None = None,
+    o_bf16: torch.Tensor | None = None,
 ) -> None:
-    """Fold key shard ``k_device`` into device ``q_device``'s running (O, lse); see bb_attn_fwd_step."""
+    """Fold key shard ``k_device`` into device ``q_device``'s running (O, lse); see bb_attn_fwd_step.
+    ``o_bf16`` (bf16, O's shape): also store bf16(O) of every row after the merge (last step)."""
     for t, name in ((q, "Q"), (k, "K"), (v, "V")):
         _require(t, torch.bfloat16, name)
     _require(o, torch.float32, "O")
     _require(lse, torch.float32, "lse")
+    if o_bf16 is not None:
+        _require(o_bf16, torch.bfloat16, "O (bf16 copy)")
+        if o_bf16.shape != o.shape:
+            raise ValueError(f"bf16 O copy has shape {tuple(o_bf16.shape)}, O has {tuple(o.shape)}")
     nq = q.shape[0] if n_q is None else n_q
     a = N.BbAttnFwdArgs(
         q=_ptr(q), k=_ptr(k), v=_ptr(v), o=_ptr(o), lse=_ptr(lse),
         n_q=nq, n_k=k.shape[0], hq=q.shape[1], hkv=k.shape[1], head_dim=q.shape[2],
         softmax_scale=float(softmax_scale), q_device=q_device, k_device=k_device,
-        layout=layout_struct(layout), mask=mask.struct,
+        layout=layout_struct(layout), mask=mask.struct, o_bf16=_ptr(o_bf16) if o_bf16 is not None else None,
     )
     N.check(N.load().bb_attn_fwd_step(C.byref(a), C.c_void_p(_stream(q.device))))
 

@@ -8,6 +8,9 @@ the B200 kernels, and the QKV projection with the layout permutation fused into 
   inverse of ``shard_token_arrays``' gather) and casts to bf16 — the shards come out of the
   projection in the layout the ring kernels read, with no separate permutation pass over HBM
   (``shard_rows``, distributed.py:104-117, is a gather of the projected matrix).
+* ``project_output_shards``: the output projection O W_attn (``AttentionParams.w_attn``) of the
+  sharded O, stored in global token order by the same permuting GEMM; the bf16 cast of O is
+  fused into the last forward step's merge epilogue (``emit_o_bf16``).
 * ``attention_forward`` / ``attention_backward`` (oracle.py:80-119): exact single-device masked
   attention through the ring-step kernels with one device (G = 1).
 
@@ -150,6 +153,59 @@ def project_qkv_shards(x, params: AttentionParams, layout: ShardLayout, heads: i
         gemm_rows(xb, w, o, rmap)
         bufs.append(o)
     return [tuple(b[i * n:(i + 1) * n].view(n, heads, d // heads) for b in bufs) for i in range(g)]
+
+
+def _w_attn_padded(params: AttentionParams, heads: int, d_pad: int, cols: int, dev: torch.device) -> torch.Tensor:
+    """W_attn as the bf16 [heads * d_pad, cols] B operand of O [n, heads * d_pad]: row h*d_pad + c
+    holds W_attn row h*d + c (c < d), padded head columns get zero rows, extra output columns
+    (TMA rows are 16-byte multiples) zeros."""
+    d = params.dim // heads
+    w = params.w_attn if isinstance(params.w_attn, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(params.w_attn, dtype=np.float64))
+    w = w.to(device=dev, dtype=torch.float32).view(heads, d, params.dim)
+    out = torch.zeros(heads, d_pad, cols, dtype=torch.float32, device=dev)
+    out[:, :d, : params.dim] = w
+    return out.view(heads * d_pad, cols).to(torch.bfloat16).contiguous()
+
+
+def project_output_shards(shards, params: AttentionParams, layout: ShardLayout, device=None) -> torch.Tensor:
+    """The output projection O W_attn of a sharded sequence (AttentionParams.w_attn,
+    oracle.py:29-44), written straight back in global token order.
+
+    ``shards``: the G ``DeviceState``s of a finished ``distributed_forward`` (their bf16 O
+    copy when it ran with ``emit_o_bf16=True`` -- the cast fused into the last step's merge
+    epilogue -- else their fp32 O, cast by ``bb_cast_pad_bf16``), or G CUDA tensors
+    [n, heads, d_pad] (bf16 or fp32) in shard order.  One tcgen05 GEMM per shard whose store
+    sends shard row r to global row ``device_token_ids(i)[r] - 1`` (``bb_gemm_bf16_rows``):
+    the inverse of shard_rows' gather, with no permutation pass.  Returns bf16 [N, dim]."""
+    if len(shards) != layout.devices:
+        raise ValueError(f"{len(shards)} shards for a layout of {layout.devices} devices")
+    tensors = []
+    for s in shards:
+        t = getattr(s, "o16", None) if hasattr(s, "o") else s
+        if t is None:
+            if s.o is None:
+                raise RuntimeError("project_output_shards requires a completed forward pass (O missing)")
+            t = s.o
+        tensors.append(t)
+    dev = _device(device) if device is not None else tensors[0].device
+    n, heads, d_pad = tensors[0].shape
+    if params.dim % heads:
+        raise ValueError(f"dim {params.dim} does not split into {heads} heads")
+    if params.dim // heads > d_pad:
+        raise ValueError(f"shards hold {d_pad} columns per head, params need {params.dim // heads}")
+    cols = -(-params.dim // 8) * 8
+    w = _w_attn_padded(params, heads, d_pad, cols, dev)
+    out = torch.empty(layout.seq_len, cols, dtype=torch.bfloat16, device=dev)
+    for i, t in enumerate(tensors):
+        if t.shape != (n, heads, d_pad) or t.shape[0] != layout.shard_size:
+            raise ValueError(f"shard {i + 1} has shape {tuple(t.shape)}, expected ({layout.shard_size}, {heads}, {d_pad})")
+        t = t.to(dev)
+        if t.dtype == torch.float32:
+            t = K.cast_pad_bf16(t.contiguous(), d_pad)
+        rows = torch.from_numpy(device_token_ids(layout, i + 1) - 1).to(dev)
+        gemm_rows(t.contiguous().view(n, heads * d_pad), w, out, rows)
+    return out[:, : params.dim]
 
 
 def _first_empty_row(mask: MaskSpec, nq: int, nk: int) -> int | None:

@@ -226,10 +226,15 @@ class ProcessRing:
 
     # -------------------------------------------------------------- forward
     def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor | None = None,
-                lse: torch.Tensor | None = None, n_q: int | None = None):
+                lse: torch.Tensor | None = None, n_q: int | None = None, o16: torch.Tensor | None = None):
         """Ring forward.  ``n_q`` < n runs only the first n_q query rows (the rows a
-        sequence-selective checkpoint dropped, see ``recompute``); K/V still circulate whole."""
+        sequence-selective checkpoint dropped, see ``recompute``); K/V still circulate whole.
+        ``o16`` (bf16, O's shape): the last launched step also stores bf16(O) there -- the
+        operand of the output projection (``layer.project_output_shards``), cast in the
+        merge epilogue instead of a separate pass."""
         n, hq, d = q.shape
+        if o16 is not None and n_q is not None and n_q < n:
+            raise ValueError("o16 is not supported with a partial (n_q < n) forward")
         if n_q is not None and n_q < n:
             o_full = torch.zeros(n, hq, d, dtype=torch.float32, device=q.device) if o is None else o
             lse_full = torch.full((hq, n), float("-inf"), device=q.device) if lse is None else lse
@@ -243,8 +248,11 @@ class ProcessRing:
             return o_full, lse_full
         o = torch.zeros(n, hq, d, dtype=torch.float32, device=q.device) if o is None else o.zero_()
         lse = torch.full((hq, n), float("-inf"), device=q.device) if lse is None else lse.fill_(float("-inf"))
+        last = max((t for t in range(self.world) if self.counts[self.rank, self.order[t]]), default=-1)
+        if o16 is not None and last < 0 and self.compute:  # nothing visible to this rank: O stays 0
+            o16.zero_()
         if self.transport == "ce" and self.world > 1:
-            self._forward_ce(q, k, v, o, lse, d)
+            self._forward_ce(q, k, v, o, lse, d, o16, last)
             return o, lse
         bufs = [(k, v)] + [(torch.empty_like(k), torch.empty_like(v)) for _ in range(2)]
         pending = None
@@ -261,7 +269,7 @@ class ProcessRing:
                 pending = self._exchange([k, v], list(nxt), dst, src)
             if self.counts[self.rank, j]:
                 self._launch(K.attn_fwd_step, q, kv[0], kv[1], o, lse, self.layout, self.dmask, self.rank + 1, j + 1,
-                             self._scale(d), n_q=q.shape[0])
+                             self._scale(d), n_q=q.shape[0], o_bf16=o16 if t == last else None)
         return o, lse
 
     def recompute(self, q, k, v, o, lse, policy) -> int:
@@ -417,7 +425,7 @@ class ProcessRing:
             self._push(ch, s, list(payload), xs, self._xs_lanes[0], f"{ch.name} step {s}")
         self.stats.bytes_sent += (self.world - 1) * ch.payload_bytes
 
-    def _forward_ce(self, q, k, v, o, lse, d):
+    def _forward_ce(self, q, k, v, o, lse, d, o16=None, last=-1):
         cs, xs, _ = self._streams()
         ch = self._channel("kv", (k, v), grad=False)
         self._push_all(ch, (k, v), cs, xs)
@@ -426,7 +434,8 @@ class ProcessRing:
             kv = (k, v) if t == 0 else ch.wait(t, cs)
             if self.counts[self.rank, j]:
                 self._launch(K.attn_fwd_step, q, kv[0], kv[1], o, lse, self.layout, self.dmask, self.rank + 1, j + 1,
-                             self._scale(d), n_q=q.shape[0], label=f"forward q{self.rank + 1} x k{j + 1}")
+                             self._scale(d), n_q=q.shape[0], o_bf16=o16 if t == last else None,
+                             label=f"forward q{self.rank + 1} x k{j + 1}")
             if t > 0:
                 ch.release(t, cs)
         cs.wait_stream(xs)

@@ -135,3 +135,32 @@ def test_projected_shards_feed_the_ring_kernels(kind):
         rows = device_token_ids(layout, i + 1) - 1
         assert np.abs(o[:, 0].double().cpu().numpy() - o_ref[rows]).max() < 1e-2
         assert np.abs(lse[0].double().cpu().numpy() - lse_ref[rows]).max() < 2e-3
+
+
+@pytest.mark.parametrize("kind,heads,d", [("zigzag", 2, 64), ("block_striped", 2, 100), ("striped", 4, 128)])
+def test_output_projection_of_the_ring_forward(kind, heads, d):
+    """O W_attn (AttentionParams.w_attn): the forward's last step stores bf16(O)
+    (bit-exact against casting the fp32 O it just merged), and project_output_shards writes
+    bf16(O) W_attn back in global token order from the shards -- against the same product in
+    float64 on the host, and identical whether it starts from the fused bf16 copy or casts O."""
+    import paper_2509_19836_b200 as bb
+
+    n, g = 2048, 4
+    dim = heads * d
+    layout = ShardLayout(kind, n, g, 64 if kind == "block_striped" else None)
+    rng = np.random.default_rng(dim)
+    q, k, v = (rng.uniform(-1, 1, (n, heads, d)) for _ in range(3))
+    p = _params(dim, 11)
+    st = bb.make_device_states(layout, q, k, v, devices=["cuda:0"] * g)
+    bb.distributed_forward(st, layout, causal_mask(), emit_o_bf16=True)
+    for s in st:
+        assert torch.equal(s.o16, s.o.to(torch.bfloat16))
+    out = bb.project_output_shards(st, p, layout)
+    assert out.shape == (n, dim) and out.dtype == torch.bfloat16
+    o_glob = bb.gather_rows(layout, [s.o16 for s in st]).double().cpu().numpy()[..., :d].reshape(n, dim)
+    ref = o_glob @ np.asarray(p.w_attn)
+    got = out.double().cpu().numpy()
+    assert np.abs(got - ref).max() <= 1e-2 * np.abs(ref).max()
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 4e-3
+    out32 = bb.project_output_shards([s.o for s in st], p, layout)
+    assert torch.equal(out32, out)

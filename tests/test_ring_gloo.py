@@ -36,7 +36,7 @@ class FakeKernels:
         a = O.allowed(self.mask, self.ids(qdev)[:nq], self.ids(kdev)[:nk])
         return torch.from_numpy(a)
 
-    def attn_fwd_step(self, q, k, v, o, lse, layout, dmask, qdev, kdev, scale, n_q=None):
+    def attn_fwd_step(self, q, k, v, o, lse, layout, dmask, qdev, kdev, scale, n_q=None, o_bf16=None):
         nq, nk = q.shape[0], k.shape[0]
         rep = q.shape[1] // k.shape[1]
         am = self._allowed(qdev, kdev, nq, nk)
@@ -51,6 +51,8 @@ class FakeKernels:
         w_o = torch.exp(lse - l_new).nan_to_num(0.0).t()[..., None]
         o.copy_(w_s * o_step + w_o * o)
         lse.copy_(l_new)
+        if o_bf16 is not None:  # (a float32 stand-in for the bf16 copy: the fakes run in float64)
+            o_bf16.copy_(o)
 
     def bwd_preprocess(self, do, o, delta):
         delta.copy_((do * o).sum(-1).t())
@@ -96,7 +98,9 @@ def _worker(rank, world, port, case, out_q):
         q, k, v, do = (torch.from_numpy(rng.uniform(-1, 1, (n, h, d))) for h in (hq, hkv, hkv, hq))
         rows = torch.from_numpy(device_token_ids(layout, rank + 1) - 1)
         ring = R.ProcessRing(layout, mask, Topology(*topo), head_dim=d)
-        o, lse = ring.forward(q[rows].contiguous(), k[rows].contiguous(), v[rows].contiguous())
+        o16 = torch.full((rows.shape[0], hq, d), float("nan"), dtype=torch.float32)
+        o, lse = ring.forward(q[rows].contiguous(), k[rows].contiguous(), v[rows].contiguous(), o16=o16)
+        assert torch.equal(o16, o.float())  # the last launched step leaves the copy of the final O
         dq, dk, dv = ring.backward(q[rows].contiguous(), k[rows].contiguous(), v[rows].contiguous(),
                                    do[rows].contiguous(), o, lse, kind=backward)
         # sequence-selective checkpoint: drop (O, lse) of rows with id <= N/2, recompute them

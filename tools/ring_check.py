@@ -67,7 +67,11 @@ def main():
                     traced = transport == "ce" and rep == 1
                     if traced:  # measured timeline of the second pass (validated on assembly)
                         ring.trace_begin()
-                    o, lse = ring.forward(q, k, v)
+                    o16 = torch.empty(q.shape, dtype=torch.bfloat16, device=dev)
+                    o, lse = ring.forward(q, k, v, o16=o16)
+                    if not torch.equal(o16, o.to(torch.bfloat16)):  # bf16 O from the last step's epilogue
+                        print(f"rank {rank} FAIL bf16 O copy differs from bf16(O)", flush=True)
+                        failures += 1
                     dq, dk, dv = ring.backward(q, k, v, do, o, lse, kind=backward)
                     if traced:
                         tl = ring.trace_collect()
