@@ -153,6 +153,18 @@ int bb_attn_bwd_preprocess(const void* dout, const float* o, float* delta, int64
 int bb_permute_rows(void* dst, const void* src, const int64_t* index, int64_t n_rows,
                     int64_t row_bytes, int32_t scatter, void* stream);
 
+/* Fill `count` 32-bit words (count % 4 == 0, 16-byte aligned) with `value`: the zeroed
+ * gradient accumulators and the -inf running lse of a ring pass (distributed.py:172-173,
+ * 270-272), at the copy rate of cudaMemsetAsync. */
+int bb_fill_u32(void* dst, uint32_t value, int64_t count, void* stream);
+
+/* dst[r, c] += src[r, c] for r < rows, c < cols over row strides dst_ld / src_ld (floats;
+ * cols and strides multiples of 4, 16-byte aligned): folding a gradient partial that
+ * arrived from a peer into the owner's accumulator (distributed.py:293-295, the
+ * circulating dQ's additions), whole or restricted to a head range. */
+int bb_add_rows_f32(float* dst, const float* src, int64_t rows, int64_t cols, int64_t dst_ld, int64_t src_ld,
+                    void* stream);
+
 /* Cast f32 -> bf16 with optional zero padding of the last dimension
  * (cols_in -> cols_out, cols_out >= cols_in); rows are contiguous. */
 int bb_cast_pad_bf16(void* dst, const float* src, int64_t rows, int32_t cols_in, int32_t cols_out,

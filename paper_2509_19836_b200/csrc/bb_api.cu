@@ -104,6 +104,8 @@ int num_sms() {
 int launch_preprocess(const void*, const float*, float*, int64_t, int32_t, int32_t, cudaStream_t);
 int launch_permute(void*, const void*, const int64_t*, int64_t, int64_t, int, cudaStream_t);
 int launch_cast_pad(void*, const float*, int64_t, int32_t, int32_t, cudaStream_t);
+int launch_fill_u32(void*, uint32_t, int64_t, cudaStream_t);
+int launch_add_rows(float*, const float*, int64_t, int64_t, int64_t, int64_t, cudaStream_t);
 int launch_lmhead_reduce(const float*, const float*, const float*, int64_t, int32_t, float*, float*,
                          cudaStream_t);
 int launch_lmhead_dlogits(const float*, const float*, const int64_t*, int64_t, int64_t, int64_t, void*,
@@ -196,6 +198,15 @@ int bb_attn_bwd_preprocess(const void* dout, const float* o, float* delta, int64
 int bb_permute_rows(void* dst, const void* src, const int64_t* index, int64_t n_rows, int64_t row_bytes,
                     int32_t scatter, void* stream) {
   return launch_permute(dst, src, index, n_rows, row_bytes, scatter, static_cast<cudaStream_t>(stream));
+}
+
+int bb_fill_u32(void* dst, uint32_t value, int64_t count, void* stream) {
+  return launch_fill_u32(dst, value, count, static_cast<cudaStream_t>(stream));
+}
+
+int bb_add_rows_f32(float* dst, const float* src, int64_t rows, int64_t cols, int64_t dst_ld, int64_t src_ld,
+                    void* stream) {
+  return launch_add_rows(dst, src, rows, cols, dst_ld, src_ld, static_cast<cudaStream_t>(stream));
 }
 
 int bb_cast_pad_bf16(void* dst, const float* src, int64_t rows, int32_t cols_in, int32_t cols_out,

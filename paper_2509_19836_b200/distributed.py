@@ -331,8 +331,8 @@ def distributed_forward(
     g = layout.devices
     ex = _exec or _Executor(states, overlap=(schedule is None or schedule.kind != "none"), record=False)
     for st in states:
-        st.o = torch.zeros(st.q.shape, dtype=torch.float32, device=st.device)
-        st.lse = torch.full((st.q.shape[1], st.q.shape[0]), float("-inf"), device=st.device)
+        st.o = K.fill_(torch.empty(st.q.shape, dtype=torch.float32, device=st.device))
+        st.lse = K.fill_(torch.empty(st.q.shape[1], st.q.shape[0], device=st.device), float("-inf"))
     masks = {st.device: K.device_mask(mask, st.device) for st in states}
     last = [max((t for t in range(g) if counts[i, order[i][t]]), default=-1) for i in range(g)]
     for i, st in enumerate(states):
@@ -413,9 +413,9 @@ def burst_backward(
         st.d_vec = torch.empty_like(st.lse)
         with torch.cuda.device(st.device):
             K.bwd_preprocess(do_i, st.o, st.d_vec)
-        st.dk = torch.zeros(st.k.shape, dtype=torch.float32, device=st.device)
-        st.dv = torch.zeros(st.v.shape, dtype=torch.float32, device=st.device)
-        st.dq = torch.zeros(st.q.shape, dtype=torch.float32, device=st.device)
+        st.dk = K.fill_(torch.empty(st.k.shape, dtype=torch.float32, device=st.device))
+        st.dv = K.fill_(torch.empty(st.v.shape, dtype=torch.float32, device=st.device))
+        st.dq = K.fill_(torch.empty(st.q.shape, dtype=torch.float32, device=st.device))
     for t in range(g):
         for i, st in enumerate(states):
             j = plan.visit[i][t]
@@ -424,7 +424,7 @@ def burst_backward(
             src = states[j]
             q_j, do_j, lse_j, d_j = ex.fetch((src.q, dos[j], src.lse, src.d_vec), st.device, j, i, f"bwd step {t + 1} q {j + 1}->{i + 1}")
             local = src.dq.device == st.device
-            dq_acc = src.dq if local else torch.zeros(src.q.shape, dtype=torch.float32, device=st.device)
+            dq_acc = src.dq if local else K.fill_(torch.empty(src.q.shape, dtype=torch.float32, device=st.device))
             ex.compute(
                 i,
                 f"bwd step {t + 1} shard {j + 1}",
@@ -435,7 +435,7 @@ def burst_backward(
             if not local:
                 (back,) = ex.fetch((dq_acc,), src.device, i, j, f"bwd step {t + 1} dq {i + 1}->{j + 1}")
                 with torch.cuda.device(src.device):
-                    src.dq.add_(back)
+                    K.add_rows_(src.dq, back)
     log = message_log_for(plan, step_payload_elements(BURST_BACKWARD, layout.seq_len, states[0].head_dim, g))
     log.bytes_moved = list(ex.bytes)
     return log
@@ -464,9 +464,9 @@ def ring_backward(
         st.d_vec = torch.empty_like(st.lse)
         with torch.cuda.device(st.device):
             K.bwd_preprocess(do_i, st.o, st.d_vec)
-        st.dq = torch.zeros(st.q.shape, dtype=torch.float32, device=st.device)
-        st.dk = torch.zeros(st.k.shape, dtype=torch.float32, device=st.device)
-        st.dv = torch.zeros(st.v.shape, dtype=torch.float32, device=st.device)
+        st.dq = K.fill_(torch.empty(st.q.shape, dtype=torch.float32, device=st.device))
+        st.dk = K.fill_(torch.empty(st.k.shape, dtype=torch.float32, device=st.device))
+        st.dv = K.fill_(torch.empty(st.v.shape, dtype=torch.float32, device=st.device))
     for t in range(g):
         for i, st in enumerate(states):
             j = plan.visit[i][t]
@@ -475,8 +475,8 @@ def ring_backward(
             src = states[j]
             k_j, v_j = ex.fetch((src.k, src.v), st.device, j, i, f"rbwd step {t + 1} kv {j + 1}->{i + 1}")
             local = src.dk.device == st.device
-            dk_acc = src.dk if local else torch.zeros(src.k.shape, dtype=torch.float32, device=st.device)
-            dv_acc = src.dv if local else torch.zeros(src.v.shape, dtype=torch.float32, device=st.device)
+            dk_acc = src.dk if local else K.fill_(torch.empty(src.k.shape, dtype=torch.float32, device=st.device))
+            dv_acc = src.dv if local else K.fill_(torch.empty(src.v.shape, dtype=torch.float32, device=st.device))
             ex.compute(
                 i,
                 f"rbwd step {t + 1} shard {j + 1}",
@@ -487,8 +487,8 @@ def ring_backward(
             if not local:
                 back_k, back_v = ex.fetch((dk_acc, dv_acc), src.device, i, j, f"rbwd step {t + 1} dkv {i + 1}->{j + 1}")
                 with torch.cuda.device(src.device):
-                    src.dk.add_(back_k)
-                    src.dv.add_(back_v)
+                    K.add_rows_(src.dk, back_k)
+                    K.add_rows_(src.dv, back_v)
     log = message_log_for(plan, step_payload_elements(RING_BACKWARD, layout.seq_len, states[0].head_dim, g))
     log.bytes_moved = list(ex.bytes)
     return log

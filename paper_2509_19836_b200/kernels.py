@@ -10,6 +10,7 @@ from __future__ import annotations
 import ctypes as C
 import hashlib
 import math
+import struct
 from collections import OrderedDict
 from dataclasses import dataclass
 
@@ -181,6 +182,44 @@ def permute_rows(dst: torch.Tensor, src: torch.Tensor, index: torch.Tensor, scat
     N.check(
         N.load().bb_permute_rows(_ptr(dst), _ptr(src), _ptr(index), rows, row_bytes, int(scatter), C.c_void_p(_stream(src.device)))
     )
+
+
+def fill_(t: torch.Tensor, value: float = 0.0) -> torch.Tensor:
+    """In-place fill of a contiguous fp32 tensor (bb_fill_u32); returns ``t``."""
+    _require(t, torch.float32, "fill target")
+    bits = struct.unpack("<I", struct.pack("<f", value))[0]
+    N.check(N.load().bb_fill_u32(_ptr(t), bits, t.numel(), C.c_void_p(_stream(t.device))))
+    return t
+
+
+def _row_view(t: torch.Tensor, name: str) -> tuple[int, int, int]:
+    """(rows, cols, row stride) of a tensor whose rows are contiguous runs (t[r] dense)."""
+    inner = 1
+    for size, stride in zip(reversed(t.shape[1:]), reversed(t.stride()[1:])):
+        if size != 1 and stride != inner:
+            raise ValueError(f"{name}: every row must be one contiguous run")
+        inner *= size
+    return t.shape[0], inner, t.stride(0) if t.dim() > 1 else inner
+
+
+def add_rows_(dst: torch.Tensor, src: torch.Tensor) -> torch.Tensor:
+    """dst += src for fp32 tensors of one shape whose rows are contiguous runs (a whole
+    accumulator or a head range ``x[:, a:b]`` of one), on bb_add_rows_f32; returns ``dst``."""
+    _require_cuda_f32(dst, "fold target")
+    _require_cuda_f32(src, "fold source")
+    if dst.shape != src.shape:
+        raise ValueError(f"fold shapes differ: {tuple(dst.shape)} vs {tuple(src.shape)}")
+    rows, cols, dld = _row_view(dst, "fold target")
+    _, _, sld = _row_view(src, "fold source")
+    N.check(N.load().bb_add_rows_f32(_ptr(dst), _ptr(src), rows, cols, dld, sld, C.c_void_p(_stream(dst.device))))
+    return dst
+
+
+def _require_cuda_f32(t: torch.Tensor, name: str) -> None:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback), got {t.device}")
+    if t.dtype != torch.float32:
+        raise ValueError(f"{name} must be torch.float32, got {t.dtype}")
 
 
 def cast_pad_bf16(src: torch.Tensor, cols_out: int) -> torch.Tensor:

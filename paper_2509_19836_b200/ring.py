@@ -236,8 +236,8 @@ class ProcessRing:
         if o16 is not None and n_q is not None and n_q < n:
             raise ValueError("o16 is not supported with a partial (n_q < n) forward")
         if n_q is not None and n_q < n:
-            o_full = torch.zeros(n, hq, d, dtype=torch.float32, device=q.device) if o is None else o
-            lse_full = torch.full((hq, n), float("-inf"), device=q.device) if lse is None else lse
+            o_full = K.fill_(torch.empty(n, hq, d, dtype=torch.float32, device=q.device)) if o is None else o
+            lse_full = K.fill_(torch.empty(hq, n, device=q.device), float("-inf")) if lse is None else lse
             saved = self.compute
             self.compute = saved and n_q > 0  # the exchanges are collective: always run them
             try:
@@ -246,8 +246,12 @@ class ProcessRing:
                 self.compute = saved
             lse_full[:, :n_q].copy_(lse_p)
             return o_full, lse_full
-        o = torch.zeros(n, hq, d, dtype=torch.float32, device=q.device) if o is None else o.zero_()
-        lse = torch.full((hq, n), float("-inf"), device=q.device) if lse is None else lse.fill_(float("-inf"))
+        o = torch.empty(n, hq, d, dtype=torch.float32, device=q.device) if o is None else o
+        lse = torch.empty(hq, n, device=q.device) if lse is None else lse
+        # the running state's initialisation (distributed.py:172-173) is compute-lane work that
+        # one GPU does too: launched (and traced) like the kernels, skipped with them
+        self._launch(K.fill_, o, label="init O")
+        self._launch(K.fill_, lse, float("-inf"), label="init lse")
         last = max((t for t in range(self.world) if self.counts[self.rank, self.order[t]]), default=-1)
         if o16 is not None and last < 0 and self.compute:  # nothing visible to this rank: O stays 0
             o16.zero_()
@@ -288,9 +292,11 @@ class ProcessRing:
         n, hq, d = q.shape
         delta = torch.empty_like(lse)
         self._launch(K.bwd_preprocess, do, o, delta)
-        dq = torch.zeros(q.shape, dtype=torch.float32, device=q.device) if dq is None else dq.zero_()
-        dk = torch.zeros(k.shape, dtype=torch.float32, device=q.device) if dk is None else dk.zero_()
-        dv = torch.zeros(v.shape, dtype=torch.float32, device=q.device) if dv is None else dv.zero_()
+        dq = torch.empty(q.shape, dtype=torch.float32, device=q.device) if dq is None else dq
+        dk = torch.empty(k.shape, dtype=torch.float32, device=q.device) if dk is None else dk
+        dv = torch.empty(v.shape, dtype=torch.float32, device=q.device) if dv is None else dv
+        for t, name in ((dq, "dQ"), (dk, "dK"), (dv, "dV")):
+            self._launch(K.fill_, t, label=f"init {name}")
         ce = self.transport == "ce" and self.world > 1
         if kind == BURST_BACKWARD:
             (self._burst_ce if ce else self._burst)(q, k, v, do, lse, delta, dq, dk, dv, d)
@@ -324,9 +330,9 @@ class ProcessRing:
                 if grad_pending is not None and grad_pending[1] is acc:
                     for w in grad_pending[0]:
                         w.wait()
-                    dq.add_(grad_pending[2])
+                    K.add_rows_(dq, grad_pending[2])
                     grad_pending = None
-                acc.zero_()
+                K.fill_(acc)
             if self.counts[j, self.rank]:
                 self._launch(K.attn_bwd_step, payload[0], k, v, payload[1], payload[2], payload[3], acc, dk, dv,
                              self.layout, self.dmask, j + 1, self.rank + 1, self._scale(d))
@@ -335,14 +341,14 @@ class ProcessRing:
                 if grad_pending is not None:
                     for w in grad_pending[0]:
                         w.wait()
-                    dq.add_(grad_pending[2])
+                    K.add_rows_(dq, grad_pending[2])
                 box = inbox[t % 2]
                 works = self._exchange([acc], [box], j, self._who_had_me(t))
                 grad_pending = (works, acc, box)
         if grad_pending is not None:
             for w in grad_pending[0]:
                 w.wait()
-            dq.add_(grad_pending[2])
+            K.add_rows_(dq, grad_pending[2])
 
     def _ringbwd(self, q, k, v, do, lse, delta, dq, dk, dv, d):
         own = (k, v)
@@ -368,11 +374,11 @@ class ProcessRing:
                 if grad_pending is not None and grad_pending[1] is acc:
                     for w in grad_pending[0]:
                         w.wait()
-                    dk.add_(grad_pending[2][0])
-                    dv.add_(grad_pending[2][1])
+                    K.add_rows_(dk, grad_pending[2][0])
+                    K.add_rows_(dv, grad_pending[2][1])
                     grad_pending = None
-                acc[0].zero_()
-                acc[1].zero_()
+                K.fill_(acc[0])
+                K.fill_(acc[1])
             if self.counts[self.rank, j]:
                 self._launch(K.attn_bwd_step, q, kv[0], kv[1], do, lse, delta, dq, acc[0], acc[1],
                              self.layout, self.dmask, self.rank + 1, j + 1, self._scale(d))
@@ -380,16 +386,16 @@ class ProcessRing:
                 if grad_pending is not None:
                     for w in grad_pending[0]:
                         w.wait()
-                    dk.add_(grad_pending[2][0])
-                    dv.add_(grad_pending[2][1])
+                    K.add_rows_(dk, grad_pending[2][0])
+                    K.add_rows_(dv, grad_pending[2][1])
                 box = inbox[t % 2]
                 works = self._exchange(list(acc), list(box), j, self._who_had_me(t))
                 grad_pending = (works, acc, box)
         if grad_pending is not None:
             for w in grad_pending[0]:
                 w.wait()
-            dk.add_(grad_pending[2][0])
-            dv.add_(grad_pending[2][1])
+            K.add_rows_(dk, grad_pending[2][0])
+            K.add_rows_(dv, grad_pending[2][1])
 
     # -------------------------------------------------------------- copy-engine transport
     def _channel(self, name: str, tensors, grad: bool):
@@ -483,7 +489,7 @@ class ProcessRing:
             if self.compute:
                 with torch.cuda.stream(xg):
                     for x in acc:
-                        x.zero_()
+                        K.fill_(x)
             ev = torch.cuda.Event()
             ev.record(xg)
             free[t % 2] = ev
@@ -495,9 +501,9 @@ class ProcessRing:
                 with torch.cuda.stream(xf):
                     for x, g, h in zip(own_acc, views, hs):
                         if t == last and split:
-                            x[:, :h].add_(g[:, :h])  # half B is being written by the own kernel
+                            K.add_rows_(x[:, :h], g[:, :h])  # half B is being written by the own kernel
                         else:
-                            x.add_(g)
+                            K.add_rows_(x, g)
             if not (t == last and split):
                 gch.release(t, xf)
         if split:
@@ -510,7 +516,7 @@ class ProcessRing:
                 views = gch.views(last)
                 if self.compute:
                     for x, g, h in zip(own_acc, views, hs):
-                        x[:, h:].add_(g[:, h:])
+                        K.add_rows_(x[:, h:], g[:, h:])
                 gch.release(last, cs)
         cs.wait_stream(xf)
         cs.wait_stream(xs)

@@ -185,3 +185,25 @@ def test_bwd_kv_head_halves_equal_full_step():
     res = subprocess.run([sys.executable, str(root / "tools" / "bwd_heads_check.py")], capture_output=True, text=True,
                          timeout=300, env=dict(os.environ, PYTHONPATH=str(root)))
     assert res.returncode == 0 and "OK" in res.stdout, res.stdout[-2000:] + res.stderr[-2000:]
+
+
+def test_fill_and_fold_kernels(cuda):
+    """bb_fill_u32 / bb_add_rows_f32 (the ring's accumulator initialisation and gradient
+    folds): exact against torch, on whole tensors and on head-range views."""
+    x = torch.empty(1000, 6, 36, device="cuda")
+    assert bool(torch.isneginf(K.fill_(x, float("-inf"))).all())
+    assert not K.fill_(x).any()
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn(333, 8, 64, device="cuda", generator=g)
+    b = torch.randn(333, 8, 64, device="cuda", generator=g)
+    ref = a.clone()
+    ref[:, 2:5] += b[:, 2:5]
+    K.add_rows_(a[:, 2:5], b[:, 2:5])
+    assert torch.equal(a, ref)
+    ref += b
+    K.add_rows_(a, b)
+    assert torch.equal(a, ref)
+    with pytest.raises(ValueError):
+        K.add_rows_(a[:, :, :10], b[:, :, :10])  # rows are not contiguous runs
+    with pytest.raises(ValueError):
+        K.fill_(torch.empty(3, device="cuda"))  # not a multiple of 4 words

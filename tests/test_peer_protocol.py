@@ -145,6 +145,12 @@ class FakeK:
     def bwd_preprocess(self, *a, **kw):
         self._kernel()
 
+    def fill_(self, t, value=0.0):
+        return t.fill_(value)
+
+    def add_rows_(self, dst, src):
+        return dst.add_(src)
+
 
 def _arena(addr):
     base = addr & ~((1 << 32) - 1)

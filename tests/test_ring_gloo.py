@@ -57,6 +57,12 @@ class FakeKernels:
     def bwd_preprocess(self, do, o, delta):
         delta.copy_((do * o).sum(-1).t())
 
+    def fill_(self, t, value=0.0):
+        return t.fill_(value)
+
+    def add_rows_(self, dst, src):
+        return dst.add_(src)
+
     def attn_bwd_step(self, q, k, v, do, lse, delta, dq, dk, dv, layout, dmask, qdev, kdev, scale):
         rep = q.shape[1] // k.shape[1]
         am = self._allowed(qdev, kdev, q.shape[0], k.shape[0])

@@ -17,6 +17,7 @@ ap.add_argument("--heads", type=int, default=32)
 ap.add_argument("--d", type=int, default=128)
 ap.add_argument("--mask", default="causal")
 ap.add_argument("--iters", type=int, default=3)
+ap.add_argument("--halves", action="store_true", help="also time the bwd step split by kv heads (A, B, B, A)")
 args = ap.parse_args()
 
 dev = torch.device("cuda:0")
@@ -63,3 +64,13 @@ for name, fn, flops in (("fwd", fwd, 4 * d * h * pairs), ("bwd", bwd, 10 * d * h
         ts.append(a.elapsed_time(b) / 1e3)
     t = min(ts)
     print(f"{name}: {t*1e3:.2f} ms  {flops/t/1e12:.1f} TFLOP/s  (n={n} h={h} d={d} {args.mask})", flush=True)
+
+if args.halves:  # the ring's own-step split: is half B as fast as half A on its own?
+    K.bwd_preprocess(do, o, delta)
+    for heads in ((0, h // 2), (h // 2, h), (h // 2, h), (0, h // 2)):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        K.attn_bwd_step(q, k, v, do, lse, delta, dq, dk, dv, layout, dm, 1, 1, scale, kv_heads=heads)
+        b.record()
+        torch.cuda.synchronize()
+        print(f"bwd kv heads {heads}: {a.elapsed_time(b):.2f} ms", flush=True)
