@@ -188,7 +188,8 @@ def fill_(t: torch.Tensor, value: float = 0.0) -> torch.Tensor:
     """In-place fill of a contiguous fp32 tensor (bb_fill_u32); returns ``t``."""
     _require(t, torch.float32, "fill target")
     bits = struct.unpack("<I", struct.pack("<f", value))[0]
-    N.check(N.load().bb_fill_u32(_ptr(t), bits, t.numel(), C.c_void_p(_stream(t.device))))
+    with torch.cuda.device(t.device):
+        N.check(N.load().bb_fill_u32(_ptr(t), bits, t.numel(), C.c_void_p(_stream(t.device))))
     return t
 
 
@@ -211,7 +212,8 @@ def add_rows_(dst: torch.Tensor, src: torch.Tensor) -> torch.Tensor:
         raise ValueError(f"fold shapes differ: {tuple(dst.shape)} vs {tuple(src.shape)}")
     rows, cols, dld = _row_view(dst, "fold target")
     _, _, sld = _row_view(src, "fold source")
-    N.check(N.load().bb_add_rows_f32(_ptr(dst), _ptr(src), rows, cols, dld, sld, C.c_void_p(_stream(dst.device))))
+    with torch.cuda.device(dst.device):
+        N.check(N.load().bb_add_rows_f32(_ptr(dst), _ptr(src), rows, cols, dld, sld, C.c_void_p(_stream(dst.device))))
     return dst
 
 
@@ -228,7 +230,8 @@ def cast_pad_bf16(src: torch.Tensor, cols_out: int) -> torch.Tensor:
     cin = src.shape[-1]
     rows = src.numel() // max(cin, 1)
     out = torch.empty(*src.shape[:-1], cols_out, dtype=torch.bfloat16, device=src.device)
-    N.check(N.load().bb_cast_pad_bf16(_ptr(out), _ptr(src), rows, cin, cols_out, C.c_void_p(_stream(src.device))))
+    with torch.cuda.device(src.device):
+        N.check(N.load().bb_cast_pad_bf16(_ptr(out), _ptr(src), rows, cin, cols_out, C.c_void_p(_stream(src.device))))
     return out
 
 

@@ -195,16 +195,18 @@ def project_output_shards(shards, params: AttentionParams, layout: ShardLayout, 
     if params.dim // heads > d_pad:
         raise ValueError(f"shards hold {d_pad} columns per head, params need {params.dim // heads}")
     cols = -(-params.dim // 8) * 8
-    w = _w_attn_padded(params, heads, d_pad, cols, dev)
-    out = torch.empty(layout.seq_len, cols, dtype=torch.bfloat16, device=dev)
     for i, t in enumerate(tensors):
-        if t.shape != (n, heads, d_pad) or t.shape[0] != layout.shard_size:
+        if t.shape != (layout.shard_size, heads, d_pad):
             raise ValueError(f"shard {i + 1} has shape {tuple(t.shape)}, expected ({layout.shard_size}, {heads}, {d_pad})")
-        t = t.to(dev)
-        if t.dtype == torch.float32:
-            t = K.cast_pad_bf16(t.contiguous(), d_pad)
-        rows = torch.from_numpy(device_token_ids(layout, i + 1) - 1).to(dev)
-        gemm_rows(t.contiguous().view(n, heads * d_pad), w, out, rows)
+    with torch.cuda.device(dev):
+        w = _w_attn_padded(params, heads, d_pad, cols, dev)
+        out = torch.empty(layout.seq_len, cols, dtype=torch.bfloat16, device=dev)
+        for i, t in enumerate(tensors):
+            t = t.to(dev)
+            if t.dtype == torch.float32:
+                t = K.cast_pad_bf16(t.contiguous(), d_pad)
+            rows = torch.from_numpy(device_token_ids(layout, i + 1) - 1).to(dev)
+            gemm_rows(t.contiguous().view(n, heads * d_pad), w, out, rows)
     return out[:, : params.dim]
 
 
