@@ -153,7 +153,8 @@ int bb_attn_bwd_preprocess(const void* dout, const float* o, float* delta, int64
 int bb_permute_rows(void* dst, const void* src, const int64_t* index, int64_t n_rows,
                     int64_t row_bytes, int32_t scatter, void* stream);
 
-/* Fill `count` 32-bit words (count % 4 == 0, 16-byte aligned) with `value`: the zeroed
+/* Fill `count` 32-bit words (4-byte aligned; 16-byte stores when 16-byte aligned and
+ * count % 4 == 0) with `value`: the zeroed
  * gradient accumulators and the -inf running lse of a ring pass (distributed.py:172-173,
  * 270-272), at the copy rate of cudaMemsetAsync. */
 int bb_fill_u32(void* dst, uint32_t value, int64_t count, void* stream);

@@ -120,6 +120,12 @@ __global__ void fill_u32_kernel(uint4* __restrict__ dst, uint32_t v, int64_t n4)
   for (; i < n4; i += stride) dst[i] = x;
 }
 
+__global__ void fill_u32_scalar_kernel(uint32_t* __restrict__ dst, uint32_t v, int64_t n) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = v;
+}
+
 // dst[r, :cols] += src[r, :cols] over row-strided float matrices (the ring's gradient folds,
 // whole accumulators or a head range of them); 16-byte accesses, 4 in flight per thread.
 __global__ void add_rows_kernel(float4* __restrict__ dst, const float4* __restrict__ src, int64_t rows,
@@ -198,13 +204,17 @@ int launch_lmhead_dlogits(const float* logits, const float* lse, const int64_t* 
 
 int launch_fill_u32(void* dst, uint32_t value, int64_t count, cudaStream_t st) {
   if (count <= 0) return BB_OK;
-  if ((reinterpret_cast<uintptr_t>(dst) & 15) || (count & 3))
-    return set_error(BB_ERR_INVALID, "fill_u32: needs a 16-byte aligned buffer of a multiple of 4 words");
+  if (reinterpret_cast<uintptr_t>(dst) & 3) return set_error(BB_ERR_INVALID, "fill_u32: buffer not 4-byte aligned");
   int sms = 148;
   int dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t n4 = count / 4;
   const int threads = 512;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) || (count & 3)) {  // small / odd buffers: word stores
+    const int64_t blocks = std::min<int64_t>(static_cast<int64_t>(sms) * 4, (count + threads - 1) / threads);
+    fill_u32_scalar_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(static_cast<uint32_t*>(dst), value, count);
+    return check_launch("fill_u32_scalar_kernel");
+  }
+  const int64_t n4 = count / 4;
   const int64_t blocks = std::min<int64_t>(static_cast<int64_t>(sms) * 4, (n4 + threads - 1) / threads);
   fill_u32_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(static_cast<uint4*>(dst), value, n4);
   return check_launch("fill_u32_kernel");

@@ -205,5 +205,5 @@ def test_fill_and_fold_kernels(cuda):
     assert torch.equal(a, ref)
     with pytest.raises(ValueError):
         K.add_rows_(a[:, :, :10], b[:, :, :10])  # rows are not contiguous runs
-    with pytest.raises(ValueError):
-        K.fill_(torch.empty(3, device="cuda"))  # not a multiple of 4 words
+    y = torch.empty(7, 3, device="cuda")
+    assert bool((K.fill_(y[1:], 2.5) == 2.5).all())  # odd count, 4-byte aligned start: word stores
