@@ -417,6 +417,14 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       const uint32_t nxt = item_qt(w) + 1 - static_cast<uint32_t>(q_lo);  // next tile's class-table index
       const uint32_t cls_byte = nxt < nr ? cls_tab[nxt >> 2] : 0u;
       uint32_t pk[CH][16];
+      float dl[CH][32];
+      auto load_dl = [&]() {
+#pragma unroll
+        for (int c2 = 0; c2 < CH; ++c2)
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(&dl[c2][i]) = *reinterpret_cast<const float4*>(&dlt[(g * CH + c2) * 32 + i]);
+      };
       auto p_pass = [&](auto masked_tag) {
         constexpr bool MASKED = decltype(masked_tag)::value;
 #pragma unroll
@@ -424,6 +432,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           const int c = g * CH + c2;
           float s[32];
           tmem_ld32(tmem + t_lane + COL_S + c * 32, s);
+          if (c2 == CH - 1) load_dl();  // -D of both chunks: issued under the last chunk's TMEM load
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
@@ -450,12 +459,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       mbar_arrive(p_full);
       if (ct == 0) BB_PROBE(18);
       if (ct == 128) BB_PROBE(27);
-      float dl[CH][32];
-#pragma unroll
-      for (int c2 = 0; c2 < CH; ++c2)
-#pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4*>(&dl[c2][i]) = *reinterpret_cast<const float4*>(&dlt[(g * CH + c2) * 32 + i]);
       // Next item: the following query tile of the same head unless the prefetched class says
       // it is masked out (or the range ends); the general walk only then.
       int64_t w_next;
