@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       // Every shared-memory load this tile needs is issued well ahead of its first use: under the
       // SS MMAs' operand fetch (128 B/clk, the whole port) an LDS waits hundreds of cycles, and
       // the warp issues in order.  lse of both chunks now; the class byte of the next query
-      // tile now (read after the P pass); -D of both chunks right after the P pass.
+      // tile now (read after the P pass); -D of both chunks under the last S chunk's TMEM load.
       float l2[CH][32];
 #pragma unroll
       for (int c2 = 0; c2 < CH; ++c2)
