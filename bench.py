@@ -449,7 +449,7 @@ def run_gpu(args) -> None:
             # per-direction NVLink rate the ring achieves, vs 900 GB/s per direction per GPU
             "nvlink_gbs_per_direction": ring_bytes / comm_s / 1e9 if comm_s > 0 else None,
             "nvlink_peak_gbs_per_direction": 900.0,
-            "how": "max over ranks; compute = CUDA events around each attention kernel (busiest rank); comm alone = same ring with kernels off; exposed = step - compute",
+            "how": "max over ranks; compute = CUDA events around every kernel the ring launches on the compute stream (attention steps, D preprocess, accumulator init: the work one GPU also does; busiest rank); comm alone = same ring with kernels off; exposed = step - compute (exchange waits and the gradient folds)",
         }
 
     # ---- e2e through the public API with pinned host buffers.  Every step copies its
