@@ -66,6 +66,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-lmhead", action="store_true", help="skip the cfg5 fused LM-head sub-measurement")
+    ap.add_argument("--no-1m", action="store_true", help="skip the 1M-token headline sub-measurement (N >= 4 only)")
     ap.add_argument("--lm-tokens", type=int, default=131072, help="cfg5: tokens per GPU (2^20 over 8 GPUs)")
     ap.add_argument("--lm-vocab", type=int, default=131072)
     ap.add_argument("--lm-dim", type=int, default=4096)
@@ -524,6 +525,13 @@ def run_gpu(args) -> None:
         }
 
     lm = None if args.no_lmhead else run_lmhead(args, dev, world)
+    headline = None
+    if world >= 4 and not args.no_1m and args.seq != HEADLINE_SEQ:
+        del q, k, v, do, o, lse, dq, dk, dv
+        if ring.transport == "ce":
+            ring.close()  # collective: frees this run's copy-engine arenas
+        torch.cuda.empty_cache()
+        headline = run_headline_1m(args, dev, world, rank)
     e2e_api = None
     if world == 1 and not args.no_e2e:
         host = [x.float().cpu().numpy() for x in (q, k, v, do)]
@@ -583,6 +591,7 @@ def run_gpu(args) -> None:
         "ring_overlap": overlap,
         "lmhead": lm,
         "e2e_dropin_api": e2e_api,
+        "headline_1m": headline,
     }
     if lm is not None:
         lm["roofline"]["peak"] = peak
@@ -592,6 +601,92 @@ def run_gpu(args) -> None:
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+HEADLINE_SEQ = 1 << 20
+
+
+def run_headline_1m(args, dev, world: int, rank: int, steps: int = 2) -> dict:
+    """BASELINE's headline configuration itself (cfg3: 1M-token causal, zigzag, 32 heads, d=128,
+    fwd + burst bwd) on the N >= 4 GPUs of this run, as a sub-measurement of the same line: one
+    warm-up step, ``steps`` timed steps (barrier + sync on both sides, CUDA events, max over
+    ranks), then the same compute-lane / exchange-alone split as ``ring_overlap``."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_19836_b200.masks import causal_mask, unmasked_pair_count
+    from paper_2509_19836_b200.partitioning import ShardLayout
+    from paper_2509_19836_b200.ring import ProcessRing
+
+    hq = hkv = 32
+    d = 128
+    layout = ShardLayout("zigzag", HEADLINE_SEQ, world)
+    mask = causal_mask()
+    ring = ProcessRing(layout, mask, head_dim=d)
+    n = layout.shard_size
+    g = torch.Generator(device=dev).manual_seed(4321 + rank)
+
+    def rnd(h):
+        return (torch.rand(n, h, d, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
+
+    q, k, v, do = rnd(hq), rnd(hkv), rnd(hkv), rnd(hq)
+    o, lse = torch.empty(n, hq, d, device=dev), torch.empty(hq, n, device=dev)
+    dq, dk, dv = torch.empty(n, hq, d, device=dev), torch.empty(n, hkv, d, device=dev), torch.empty(n, hkv, d, device=dev)
+    flops = 14.0 * d * hq * unmasked_pair_count(mask, HEADLINE_SEQ)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        ring.forward(q, k, v, o, lse)
+        ring.backward(q, k, v, do, o, lse, dq=dq, dk=dk, dv=dv)
+
+    def timed(k_steps):
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(k_steps):
+            step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / 1e3 / k_steps
+
+    step()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        step_s = timed(steps)
+    ring.stats = type(ring.stats)()
+    ring.record = True
+    rec_s = timed(1)
+    comp_s = ring.kernel_seconds()
+    ring.record = False
+    ring.compute = False
+    comm_s = timed(1)
+    ring.compute = True
+    vals = torch.tensor([step_s, rec_s, comp_s, comm_s], device=dev, dtype=torch.float64)
+    dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    step_s, rec_s, comp_s, comm_s = (float(x) for x in vals)
+    exposed = max(0.0, rec_s - comp_s)
+    out = {
+        "config": {"workload": f"cfg3: seq {HEADLINE_SEQ} causal, zigzag layout, 32 heads (kv 32), d=128, fwd + burst_backward, ring 1x{world}",
+                   "seq_len": HEADLINE_SEQ, "heads": hq, "head_dim": d},
+        "value": flops / step_s / 1e12,
+        "unit": "TFLOPS",
+        "tflops_per_gpu": flops / step_s / 1e12 / world,
+        "mfu": flops / step_s / 1e12 / world / DENSE_BF16_PEAK,
+        "ms_per_step": step_s * 1e3,
+        "steps": steps,
+        "warmup": 1,
+        "exposed_comm_ms": exposed * 1e3,
+        "comm_alone_ms": comm_s * 1e3,
+        "hidden_frac": (1.0 - min(exposed, comm_s) / comm_s) if comm_s > 0 else None,
+        "clocks": clk.summary(),
+        "how": "timed steps: max over ranks of CUDA events on the compute stream; hidden: one extra step with "
+               "kernel events (compute lane) and one with the kernels off (exchange alone), as ring_overlap",
+    }
+    del q, k, v, do, o, lse, dq, dk, dv
+    if ring.transport == "ce":
+        ring.close()
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_dropin_e2e(args, layout, mask, host, flops_step: float, steps: int = 2) -> dict:
