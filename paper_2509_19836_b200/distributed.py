@@ -29,6 +29,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
+from . import hostio
 from . import kernels as K
 from .fabric import (
     BURST_BACKWARD,
@@ -96,7 +97,7 @@ class DeviceState:
         t = getattr(self, name)
         if t is None:
             raise RuntimeError(f"{name} has not been computed")
-        a = t.detach().float().cpu().double().numpy()  # torch's multi-threaded host cast, not NumPy's single-threaded one
+        a = hostio.to_host_f64(t)  # pinned staging + threaded host cast
         if name in ("lse", "d_vec"):
             return a[0] if self.single_head else a
         a = a[..., : self.head_dim]
@@ -120,7 +121,15 @@ def _physical_devices(g: int, devices) -> list[torch.device]:
 
 def _as_global(x, name: str, dev: torch.device) -> tuple[torch.Tensor, bool]:
     """Caller array -> CUDA tensor [N, H, d] (fp32 or bf16), plus 'was 2-D'."""
-    t = torch.as_tensor(x)
+    if isinstance(x, np.ndarray) or not isinstance(x, torch.Tensor):
+        a = np.asarray(x)
+        two_d = a.ndim == 2
+        if two_d:
+            a = a[:, None, :]
+        if a.ndim != 3:
+            raise ValueError(f"{name} must be [N, d] or [N, H, d], got shape {tuple(a.shape)}")
+        return hostio.to_device(a, dev), two_d  # float32 on the device, via pinned staging
+    t = x
     two_d = t.ndim == 2
     if two_d:
         t = t[:, None, :]
@@ -190,7 +199,23 @@ def shard_rows(layout: ShardLayout, x) -> list:
             out.append(o)
         return out
     x = np.asarray(x)
-    return [x[r - 1] for r in ids]
+    return [_take_rows(x, r - 1) for r in ids]
+
+
+def _take_rows(x: np.ndarray, rows: np.ndarray) -> np.ndarray:
+    """x[rows] (a new array, like the reference's fancy index) for the sorted runs every
+    layout's shard is made of: one block copy per run on torch's thread pool instead of
+    NumPy's single-threaded per-row gather."""
+    breaks = np.flatnonzero(np.diff(rows) != 1) + 1
+    if len(rows) == 0 or len(breaks) > 64 or not x.flags.c_contiguous or x.dtype.kind not in "fiub":
+        return x[rows]
+    starts = np.concatenate([[0], breaks]).astype(np.int64)
+    ends = np.concatenate([breaks, [len(rows)]]).astype(np.int64)
+    out = np.empty((len(rows),) + x.shape[1:], dtype=x.dtype)
+    for a, b in zip(starts, ends):
+        r0 = int(rows[a])
+        torch.from_numpy(out[a:b]).copy_(torch.from_numpy(x[r0: r0 + (b - a)]))
+    return out
 
 
 def gather_rows(layout: ShardLayout, shard_arrays: list):
@@ -374,12 +399,15 @@ def _require_forward(states: list[DeviceState], what: str) -> None:
 def _do_shards(states: list[DeviceState], do_shards) -> list[torch.Tensor]:
     out = []
     for st, d in zip(states, do_shards):
-        t = torch.as_tensor(d)
+        host = not isinstance(d, torch.Tensor)
+        t = np.asarray(d) if host else d
         if t.ndim == 2:
             t = t[:, None, :]
         if t.shape[0] != st.q.shape[0] or t.shape[1] != st.q.shape[1]:
             raise ValueError(f"dO shard for device {st.index} has shape {tuple(t.shape)}, expected {tuple(st.q.shape[:2])} x d")
-        if t.dtype not in (torch.bfloat16, torch.float32):
+        if host:
+            t = hostio.to_device(t, st.device)
+        elif t.dtype not in (torch.bfloat16, torch.float32):
             t = t.to(torch.float32)
         out.append(_to_kernel_bf16(t.to(st.device), st.q.shape[2]))
     return out

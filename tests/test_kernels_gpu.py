@@ -207,3 +207,20 @@ def test_fill_and_fold_kernels(cuda):
         K.add_rows_(a[:, :, :10], b[:, :, :10])  # rows are not contiguous runs
     y = torch.empty(7, 3, device="cuda")
     assert bool((K.fill_(y[1:], 2.5) == 2.5).all())  # odd count, 4-byte aligned start: word stores
+
+
+def test_hostio_staged_copies_are_exact(cuda):
+    """The drop-in API's host <-> device paths (pinned staging, chunked, threaded host casts):
+    identical to the plain torch conversions, across chunk boundaries (> 128 MB) and ragged ends."""
+    from paper_2509_19836_b200 import hostio
+
+    rng = np.random.default_rng(3)
+    for shape in ((3, 5, 7), (45_000_001,)):
+        x = rng.standard_normal(shape)  # float64
+        d = hostio.to_device(x, torch.device("cuda"))
+        assert d.dtype == torch.float32 and torch.equal(d.cpu(), torch.from_numpy(x).float())
+        b = hostio.to_device(x, torch.device("cuda"), torch.bfloat16)
+        assert torch.equal(b.cpu(), torch.from_numpy(x).float().to(torch.bfloat16))
+        h = hostio.to_host_f64(d)
+        assert h.dtype == np.float64 and np.array_equal(h, x.astype(np.float32).astype(np.float64))
+    assert hostio.to_host_f64(torch.empty(0, 4, device="cuda")).shape == (0, 4)

@@ -25,6 +25,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seq", type=int, default=131072)
     ap.add_argument("--heads", type=int, default=32)
+    ap.add_argument("--comm-only", action="store_true", help="trace the exchanges with the kernels off")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -48,6 +49,7 @@ def main():
         step()
     torch.cuda.synchronize()
     dist.barrier()
+    ring.compute = not args.comm_only
     ring.trace_begin()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
