@@ -29,3 +29,16 @@ def test_ring_matches_oracle(world):
     res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1200)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     assert "FAIL" not in res.stdout
+
+
+def test_headline_1m_sampled_rows_match_float64():
+    """cfg3 itself (1M tokens, causal, zigzag, 32 heads, d=128) on the 4-GPU production ring:
+    sampled O / lse / dQ / dK / dV rows against float64 (tools/parity_1m.py)."""
+    if _gpus() < 4:
+        pytest.skip(f"needs 4 GPUs, {_gpus()} visible")
+    env = dict(os.environ, PYTHONPATH=str(ROOT))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+           "--master-addr", "127.0.0.1", "--master-port", "29611", str(ROOT / "tools" / "parity_1m.py")]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1800)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    assert res.stdout.count(" ok") == 2, res.stdout[-3000:]
