@@ -723,7 +723,8 @@ def run_dropin_e2e(args, layout, mask, host, flops_step: float, steps: int = 2) 
         "d2h_bytes_per_step": sum(x.size * 4 for x in (g[0].dq, g[0].dk, g[0].dv)),
         "output_dtype": str(g[0].dq.dtype),
         "how": "NumPy float32 [N, H, d] in, float64 NumPy dQ/dK/dV out through make_device_states, distributed_forward, "
-        "burst_backward, backward_grads; host wall clock, pageable memory, conversions included",
+        "burst_backward, backward_grads; host wall clock; the caller's pageable NumPy arrays, staged through "
+        "pinned buffers by the package (hostio.py); conversions included",
     }
 
 
