@@ -13,7 +13,12 @@
  *   bb_permute_rows         distributed.py:104-130  shard_rows / gather_rows / make_device_states
  *   bb_lmhead_fused         lmhead.py:41-93         fused_lmhead_loss (loss, dH, dW)
  *   bb_gemm_bf16_rows       oracle.py:60-65 +       project_qkv with shard_rows' permutation
- *                           distributed.py:104-117  fused into the GEMM store
+ *                           distributed.py:104-117  fused into the GEMM store; also the output
+ *                           oracle.py:29-44         projection O W_attn back to token order
+ *   bb_fill_u32             distributed.py:172-173  the zero / -inf initialisation of O, lse and
+ *                           (and :270-272)          the gradient accumulators
+ *   bb_add_rows_f32         distributed.py:293-295  adding a peer's dQ (dK/dV) partial to the
+ *                                                   owner's accumulator
  *   bb_matmul_f64 ...       numerics.py:35-116      the reference's float64 tile math
  *   bb_xent_f64             oracle.py:129-154       (matmul, row_logsumexp, lse_merge,
  *                                                   exp_shifted, exp_gap, rowsum_hadamard)
