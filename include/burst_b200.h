@@ -88,7 +88,9 @@ typedef struct bb_mask {
  * running (O, lse).  Q/K/V are bf16 token-major [rows, heads, head_dim]; the
  * running state is f32 O [n_q, hq, head_dim] and lse [hq, n_q], initialised by
  * the caller to 0 / -inf (distributed.py:172-173).  Rows with no allowed key in
- * this step are left untouched (exp(-inf) identity, numerics.py:62-69). */
+ * this step are left untouched (exp(-inf) identity, numerics.py:62-69).
+ * A key shard above 524288 rows (zigzag / contiguous layouts) is run as launches over
+ * its consecutive-id sub-shards; bb_attn_bwd_step does the same for query shards. */
 typedef struct bb_attn_fwd_args {
   const void* q;
   const void* k;
@@ -264,6 +266,13 @@ const char* bb_last_error(void);
 /* Diagnostics: with BB_PROBE=1 in the environment, kernels record per-phase
  * clock64() stamps of CTA (0,0) for its first tiles; copies n int64 to host. */
 int bb_debug_probe(int64_t* host_out, int32_t n);
+/* Test hook: the shard size (rows, multiple of 128; 0 = the default 524288) above which
+ * bb_attn_fwd_step (key shard) and bb_attn_bwd_step (query shard) split a zigzag or contiguous
+ * shard into sub-shards of a contiguous layout with more devices and launch every sub-shard
+ * pair -- how one call takes a shard larger than the kernels' class tables (a 1M-token
+ * sequence on one or two GPUs).  Process-wide. */
+int bb_debug_set_split_rows(int64_t rows);
+
 /* Mask realisation dump for tests (replaces nothing in the reference; it exposes what the
  * kernels compute in place of local_pair_mask, partitioning.py:120-169).  For the ring step
  * (q_device, k_device) with n_q query and n_k key rows, writes classes[qt * n_kt + kt]

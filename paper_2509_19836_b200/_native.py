@@ -27,6 +27,7 @@ EXPORTS = (
     "bb_permute_rows",
     "bb_cast_pad_bf16",
     "bb_fill_u32",
+    "bb_debug_set_split_rows",
     "bb_add_rows_f32",
     "bb_lmhead_workspace_bytes",
     "bb_lmhead_fused",
@@ -161,6 +162,7 @@ def load(path: os.PathLike | str | None = None) -> C.CDLL:
     lib.bb_permute_rows.argtypes = [vp, vp, vp, i64, i64, i32, vp]
     lib.bb_cast_pad_bf16.argtypes = [vp, vp, i64, i32, i32, vp]
     lib.bb_fill_u32.argtypes = [vp, C.c_uint32, i64, vp]
+    lib.bb_debug_set_split_rows.argtypes = [i64]
     lib.bb_add_rows_f32.argtypes = [vp, vp, i64, i64, i64, i64, vp]
     lib.bb_lmhead_workspace_bytes.argtypes = [i64, i64, i64, i64]
     lib.bb_lmhead_workspace_bytes.restype = i64

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "bb_host.h"
 
@@ -151,6 +152,54 @@ static int validate_ring_step(const bb_layout& L, const bb_mask& M, int64_t n_q,
   return BB_OK;
 }
 
+// ---- shards larger than one launch takes (MAX_SHARD_ROWS) --------------------------------
+// A zigzag shard is two runs of consecutive token ids (chunks i and 2G+1-i of the sequence in
+// 2G chunks) and a contiguous shard one run, so both are exactly sub-shards of a contiguous
+// layout with more devices: chunk c of contiguous(N, G') is device c.  The masks read global
+// ids only, so a step over such a shard is the same math as the steps over every pair of its
+// sub-shards (the forward merges them like ring steps; the backward accumulates).  Striped
+// layouts have no such runs; they keep the per-launch limit.
+std::atomic<int64_t> g_split_rows{0};  // test hook (bb_debug_set_split_rows); 0 = MAX_SHARD_ROWS
+
+struct SubShard {
+  int32_t dev;
+  int64_t row0, rows;
+};
+
+// Sub-shards of rows [0, n) of device `dev`, as devices of contiguous(N, g_out); false when the
+// layout cannot be split this way.
+bool split_shard(const bb_layout& L, int32_t dev, int64_t n, int64_t limit, int32_t& g_out, std::vector<SubShard>& out) {
+  int64_t g0;
+  std::vector<int32_t> chunks;  // this device's chunks of contiguous(N, g0), in row order
+  if (L.kind == BB_LAYOUT_ZIGZAG) {
+    g0 = 2 * static_cast<int64_t>(L.devices);
+    chunks = {dev, static_cast<int32_t>(g0 + 1 - dev)};
+  } else if (L.kind == BB_LAYOUT_CONTIGUOUS) {
+    g0 = L.devices;
+    chunks = {dev};
+  } else {
+    return false;
+  }
+  int64_t f = 1;
+  while (L.seq_len / (g0 * f) > limit) f *= 2;
+  if (L.seq_len % (g0 * f) || g0 * f > INT32_MAX) return false;
+  const int64_t rows = L.seq_len / (g0 * f);
+  g_out = static_cast<int32_t>(g0 * f);
+  out.clear();
+  int64_t row0 = 0;
+  for (int32_t c : chunks)
+    for (int64_t k = 0; k < f && row0 < n; ++k, row0 += rows)
+      out.push_back({static_cast<int32_t>((c - 1) * f + k + 1), row0, std::min(rows, n - row0)});
+  return true;
+}
+
+int64_t split_limit() {
+  const int64_t r = g_split_rows.load();
+  return r > 0 ? r : MAX_SHARD_ROWS;
+}
+
+bool needs_split(int64_t n, int64_t limit) { return n > limit; }
+
 }  // namespace bb
 
 using namespace bb;
@@ -175,7 +224,34 @@ int bb_attn_fwd_step(const bb_attn_fwd_args* a, void* stream) {
     return rc;
   if (a->o_bf16 && (reinterpret_cast<uintptr_t>(a->o_bf16) & 15))
     return set_error(BB_ERR_INVALID, "bb_attn_fwd_step: o_bf16 must be 16-byte aligned");
-  return launch_attn_fwd(*a, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t limit = split_limit();
+  if (!needs_split(a->n_k, limit)) return launch_attn_fwd(*a, st, a->n_q);
+  int32_t gq = 0, gk = 0;
+  std::vector<SubShard> qs, ks;
+  if (!split_shard(a->layout, a->q_device, a->n_q, limit, gq, qs) || !split_shard(a->layout, a->k_device, a->n_k, limit, gk, ks))
+    return set_error(BB_ERR_UNSUPPORTED, "bb_attn_fwd_step: a key shard of %lld rows (> %lld) needs a zigzag or contiguous layout",
+                     (long long)a->n_k, (long long)limit);
+  const int64_t qrow = static_cast<int64_t>(a->hq) * a->head_dim, krow = static_cast<int64_t>(a->hkv) * a->head_dim;
+  for (const SubShard& q : qs) {
+    for (size_t i = 0; i < ks.size(); ++i) {
+      const SubShard& k = ks[i];
+      bb_attn_fwd_args b = *a;
+      b.layout = bb_layout{BB_LAYOUT_CONTIGUOUS, gq, a->layout.seq_len, 0};
+      b.q_device = q.dev;
+      b.k_device = k.dev;
+      b.n_q = q.rows;
+      b.n_k = k.rows;
+      b.q = static_cast<const char*>(a->q) + q.row0 * qrow * 2;
+      b.o = a->o + q.row0 * qrow;
+      b.lse = a->lse + q.row0;
+      b.k = static_cast<const char*>(a->k) + k.row0 * krow * 2;
+      b.v = static_cast<const char*>(a->v) + k.row0 * krow * 2;
+      b.o_bf16 = (a->o_bf16 && i + 1 == ks.size()) ? static_cast<char*>(a->o_bf16) + q.row0 * qrow * 2 : nullptr;
+      if (int rc = launch_attn_fwd(b, st, a->n_q)) return rc;
+    }
+  }
+  return BB_OK;
 }
 
 int bb_attn_bwd_step(const bb_attn_bwd_args* a, void* stream) {
@@ -186,7 +262,42 @@ int bb_attn_bwd_step(const bb_attn_bwd_args* a, void* stream) {
   if (a->kv_head_end != 0 && (a->kv_head_begin < 0 || a->kv_head_end > a->hkv || a->kv_head_begin >= a->kv_head_end))
     return set_error(BB_ERR_INVALID, "bb_attn_bwd_step: kv head range [%d, %d) outside [0, %d)", a->kv_head_begin,
                      a->kv_head_end, a->hkv);
-  return launch_attn_bwd(*a, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t limit = split_limit();
+  if (!needs_split(a->n_q, limit)) return launch_attn_bwd(*a, st, a->n_q);
+  int32_t gq = 0, gk = 0;
+  std::vector<SubShard> qs, ks;
+  if (!split_shard(a->layout, a->q_device, a->n_q, limit, gq, qs) || !split_shard(a->layout, a->k_device, a->n_k, limit, gk, ks))
+    return set_error(BB_ERR_UNSUPPORTED, "bb_attn_bwd_step: a query shard of %lld rows (> %lld) needs a zigzag or contiguous layout",
+                     (long long)a->n_q, (long long)limit);
+  const int64_t qrow = static_cast<int64_t>(a->hq) * a->head_dim, krow = static_cast<int64_t>(a->hkv) * a->head_dim;
+  for (const SubShard& k : ks) {
+    for (const SubShard& q : qs) {
+      bb_attn_bwd_args b = *a;
+      b.layout = bb_layout{BB_LAYOUT_CONTIGUOUS, gq, a->layout.seq_len, 0};
+      b.q_device = q.dev;
+      b.k_device = k.dev;
+      b.n_q = q.rows;
+      b.n_k = k.rows;
+      b.q = static_cast<const char*>(a->q) + q.row0 * qrow * 2;
+      b.dout = static_cast<const char*>(a->dout) + q.row0 * qrow * 2;
+      b.lse = a->lse + q.row0;
+      b.delta = a->delta + q.row0;
+      b.dq = a->dq + q.row0 * qrow;
+      b.k = static_cast<const char*>(a->k) + k.row0 * krow * 2;
+      b.v = static_cast<const char*>(a->v) + k.row0 * krow * 2;
+      b.dk = a->dk + k.row0 * krow;
+      b.dv = a->dv + k.row0 * krow;
+      if (int rc = launch_attn_bwd(b, st, a->n_q)) return rc;
+    }
+  }
+  return BB_OK;
+}
+
+int bb_debug_set_split_rows(int64_t rows) {
+  if (rows < 0 || rows % 128) return set_error(BB_ERR_INVALID, "bb_debug_set_split_rows: %lld is not a multiple of 128", (long long)rows);
+  g_split_rows.store(rows);
+  return BB_OK;
 }
 
 int bb_attn_bwd_preprocess(const void* dout, const float* o, float* delta, int64_t n, int32_t heads,

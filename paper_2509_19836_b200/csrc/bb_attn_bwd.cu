@@ -78,6 +78,7 @@ struct BwdParams {
   float* dk;
   float* dv;
   int64_t n_q, n_k;
+  int64_t lse_ld;  // row length of the caller's lse / delta arrays (>= n_q: a sub-shard launch)
   int32_t hq, hkv;
   int32_t kv_head0;  // first kv head of this launch (grid.y covers the range)
   float scale, scale_log2;
@@ -370,7 +371,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     auto load_vec = [&](int64_t w) {
       const int64_t r = static_cast<int64_t>(item_qt(w)) * 128 + CPG * g + (gt & 63);
       if (r >= p.n_q) return gt < 64 ? -INFINITY : 0.f;
-      return __ldg((gt < 64 ? p.lse : p.delta) + static_cast<int64_t>(item_head(w)) * p.n_q + r);
+      return __ldg((gt < 64 ? p.lse : p.delta) + static_cast<int64_t>(item_head(w)) * p.lse_ld + r);
     };
     auto store_vec = [&](float raw) {  // stored negated for the packed FFMA2 / FADD2 forms:
       vec_g[gt] = gt >= 64 ? -raw : raw == -INFINITY ? -INFINITY : -raw * 1.4426950408889634f;  // -D, -lse*log2e
@@ -615,8 +616,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 }
 
 template <int D>
-int launch_bwd_d(const bb_attn_bwd_args& a, cudaStream_t st) {
-  if ((a.n_q + 127) / 128 > MAX_QT)
+int launch_bwd_d(const bb_attn_bwd_args& a, cudaStream_t st, int64_t lse_ld) {
+  if ((a.n_q + 127) / 128 > MAX_QT)  // bb_api.cu splits larger shards before they get here
     return set_error(BB_ERR_UNSUPPORTED, "attn_bwd: query shard of %lld rows exceeds %d (raise MAX_QT)", (long long)a.n_q, MAX_QT * 128);
   CUtensorMap tq, tk, tv, tdo, tdq;
   const uint64_t qrow = static_cast<uint64_t>(a.hq) * D * 2, krow = static_cast<uint64_t>(a.hkv) * D * 2;
@@ -633,6 +634,7 @@ int launch_bwd_d(const bb_attn_bwd_args& a, cudaStream_t st) {
   p.dk = a.dk;
   p.dv = a.dv;
   p.n_q = a.n_q;
+  p.lse_ld = lse_ld;
   p.n_k = a.n_k;
   p.hq = a.hq;
   p.hkv = a.hkv;
@@ -663,9 +665,9 @@ int launch_bwd_d(const bb_attn_bwd_args& a, cudaStream_t st) {
 
 }  // namespace
 
-int launch_attn_bwd(const bb_attn_bwd_args& a, cudaStream_t st) {
-  if (a.head_dim == 128) return launch_bwd_d<128>(a, st);
-  if (a.head_dim == 64) return launch_bwd_d<64>(a, st);
+int launch_attn_bwd(const bb_attn_bwd_args& a, cudaStream_t st, int64_t lse_ld) {
+  if (a.head_dim == 128) return launch_bwd_d<128>(a, st, lse_ld);
+  if (a.head_dim == 64) return launch_bwd_d<64>(a, st, lse_ld);
   return set_error(BB_ERR_UNSUPPORTED, "attn_bwd: head_dim %d (kernels take 64 or 128)", a.head_dim);
 }
 

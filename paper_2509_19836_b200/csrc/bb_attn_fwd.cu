@@ -62,6 +62,7 @@ struct FwdParams {
   float* o;
   float* lse;
   int64_t n_q, n_k;
+  int64_t lse_ld;  // row length of the caller's lse array (>= n_q: a sub-shard launch, bb_api.cu)
   int32_t hq, hkv;
   float scale_log2;
   int32_t q_device, k_device;
@@ -398,7 +399,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       float w_step = 0.f, w_old = 0.f, lse_new = -INFINITY;
       const bool write = row_ok && lse_step != -INFINITY;
       written = write;
-      float* lse_ptr = p.lse + static_cast<int64_t>(head) * p.n_q + qrow;
+      float* lse_ptr = p.lse + static_cast<int64_t>(head) * p.lse_ld + qrow;
       if (write) {
         const float lse_prev = *lse_ptr;
         if (lse_prev == -INFINITY) {
@@ -453,8 +454,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 }
 
 template <int D>
-int launch_fwd_d(const bb_attn_fwd_args& a, cudaStream_t st) {
-  if ((a.n_k + 127) / 128 > MAX_KT)
+int launch_fwd_d(const bb_attn_fwd_args& a, cudaStream_t st, int64_t lse_ld) {
+  if ((a.n_k + 127) / 128 > MAX_KT)  // bb_api.cu splits larger shards before they get here
     return set_error(BB_ERR_UNSUPPORTED, "attn_fwd: key shard of %lld rows exceeds %d (raise MAX_KT)", (long long)a.n_k, MAX_KT * 128);
   CUtensorMap tq, tk, tv;
   const uint64_t qrow = static_cast<uint64_t>(a.hq) * D * 2, krow = static_cast<uint64_t>(a.hkv) * D * 2;
@@ -467,6 +468,7 @@ int launch_fwd_d(const bb_attn_fwd_args& a, cudaStream_t st) {
   p.lse = a.lse;
   p.n_q = a.n_q;
   p.n_k = a.n_k;
+  p.lse_ld = lse_ld;
   p.hq = a.hq;
   p.hkv = a.hkv;
   p.scale_log2 = a.softmax_scale * 1.4426950408889634f;
@@ -495,9 +497,9 @@ int launch_fwd_d(const bb_attn_fwd_args& a, cudaStream_t st) {
 
 }  // namespace
 
-int launch_attn_fwd(const bb_attn_fwd_args& a, cudaStream_t st) {
-  if (a.head_dim == 128) return launch_fwd_d<128>(a, st);
-  if (a.head_dim == 64) return launch_fwd_d<64>(a, st);
+int launch_attn_fwd(const bb_attn_fwd_args& a, cudaStream_t st, int64_t lse_ld) {
+  if (a.head_dim == 128) return launch_fwd_d<128>(a, st, lse_ld);
+  if (a.head_dim == 64) return launch_fwd_d<64>(a, st, lse_ld);
   return set_error(BB_ERR_UNSUPPORTED, "attn_fwd: head_dim %d (kernels take 64 or 128)", a.head_dim);
 }
 

@@ -51,8 +51,11 @@ int gemm_n_tile();
 int launch_gemm_bf16(const void* a, const void* b, void* c16, const int64_t* row_map, int64_t m, int64_t n, int64_t k,
                      int64_t lda, int64_t ldb, int64_t ldc, bool b_mn, cudaStream_t stream);
 
-int launch_attn_fwd(const bb_attn_fwd_args& a, cudaStream_t stream);
-int launch_attn_bwd(const bb_attn_bwd_args& a, cudaStream_t stream);
+// lse_ld: row length of the lse (and delta) arrays; a.n_q unless bb_api.cu launches a sub-shard
+int launch_attn_fwd(const bb_attn_fwd_args& a, cudaStream_t stream, int64_t lse_ld);
+int launch_attn_bwd(const bb_attn_bwd_args& a, cudaStream_t stream, int64_t lse_ld);
+// largest shard (rows) one launch takes: the kernels' class tables hold 4096 tiles of 128
+constexpr int64_t MAX_SHARD_ROWS = 4096 * 128;
 
 int launch_matmul_f64(const double* a, int64_t sa0, int64_t sa1, const double* b, int64_t sb0, int64_t sb1,
                       double* c, int64_t m, int64_t n, int64_t k, cudaStream_t st);

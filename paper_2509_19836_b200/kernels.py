@@ -184,6 +184,12 @@ def permute_rows(dst: torch.Tensor, src: torch.Tensor, index: torch.Tensor, scat
     )
 
 
+def set_split_rows(rows: int = 0) -> None:
+    """Test hook (bb_debug_set_split_rows): shard size above which one ring-step call is
+    launched as sub-shard pairs; 0 restores the default (the kernels' 524288-row tables)."""
+    N.check(N.load().bb_debug_set_split_rows(int(rows)))
+
+
 def fill_(t: torch.Tensor, value: float = 0.0) -> torch.Tensor:
     """In-place fill of a contiguous fp32 tensor (bb_fill_u32); returns ``t``."""
     _require(t, torch.float32, "fill target")

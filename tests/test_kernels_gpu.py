@@ -224,3 +224,62 @@ def test_hostio_staged_copies_are_exact(cuda):
         h = hostio.to_host_f64(d)
         assert h.dtype == np.float64 and np.array_equal(h, x.astype(np.float32).astype(np.float64))
     assert hostio.to_host_f64(torch.empty(0, 4, device="cuda")).shape == (0, 4)
+
+
+@pytest.mark.parametrize("kind,g", [("zigzag", 2), ("contiguous", 2), ("zigzag", 1)])
+@pytest.mark.parametrize("maskname", ["causal", "window", "block"])
+def test_oversized_shards_split_into_sub_shard_pairs(cuda, kind, g, maskname):
+    """A shard larger than one launch takes (the kernels' 4096-tile class tables, 524288 rows)
+    is run as the pairs of its consecutive-id sub-shards (bb_api.cu).  Forced here at 256 rows
+    (bb_debug_set_split_rows): every ring step, a prefix (n_q < shard) and the bf16 O copy must
+    match the single-launch results up to bf16 rounding of P and accumulation order."""
+    n, h, d = 4096, 2, 64
+    layout = ShardLayout(kind, n, g)
+    mask = {"causal": causal_mask(), "window": sliding_window_mask(1000),
+            "block": block_sparse_mask(np.tril(np.ones((16, 16), dtype=np.int64)) - np.tril(np.ones((16, 16), dtype=np.int64), -5), 256)}[maskname]
+    dev = torch.device("cuda")
+    dm = K.device_mask(mask, dev)
+    m = layout.shard_size
+    gen = torch.Generator(device=dev).manual_seed(9)
+    q, k, v, do = ((torch.rand(g, m, h, d, device=dev, generator=gen) * 2 - 1).to(torch.bfloat16) for _ in range(4))
+    scale = 1 / math.sqrt(d)
+
+    def run(n_q):
+        outs = []
+        for i in range(g):
+            o = torch.zeros(n_q, h, d, device=dev)
+            lse = torch.full((h, n_q), float("-inf"), device=dev)
+            o16 = torch.empty(n_q, h, d, dtype=torch.bfloat16, device=dev)
+            for j in range(g):
+                K.attn_fwd_step(q[i, :n_q].contiguous(), k[j], v[j], o, lse, layout, dm, i + 1, j + 1, scale, n_q=n_q,
+                                o_bf16=o16 if j == g - 1 else None)
+            assert torch.equal(o16, o.to(torch.bfloat16))
+            delta = torch.empty(h, n_q, device=dev)
+            dq = torch.zeros(n_q, h, d, device=dev)
+            dk, dv = torch.zeros(m, h, d, device=dev), torch.zeros(m, h, d, device=dev)
+            K.bwd_preprocess(do[i, :n_q].contiguous(), o, delta)
+            for j in range(g):
+                dkj, dvj = torch.zeros(m, h, d, device=dev), torch.zeros(m, h, d, device=dev)
+                K.attn_bwd_step(q[i, :n_q].contiguous(), k[j], v[j], do[i, :n_q].contiguous(), lse, delta, dq, dkj, dvj,
+                                layout, dm, i + 1, j + 1, scale)
+                dk += dkj
+                dv += dvj
+            outs.append((o, lse, dq, dk, dv))
+        return outs
+
+    for n_q in (m, 1000):
+        ref = run(n_q)
+        try:
+            K.set_split_rows(256)
+            got = run(n_q)
+        finally:
+            K.set_split_rows(0)
+        for a, b in zip(got, ref):
+            for x, y, name in zip(a, b, ("o", "lse", "dq", "dk", "dv")):
+                fin = torch.isfinite(y)
+                assert torch.equal(torch.isfinite(x), fin), name
+                err = float((x[fin] - y[fin]).abs().max()) / max(float(y[fin].abs().max()), 1e-30)
+                # P is rounded to bf16 against each launch's own running max, so O and the
+                # gradients move at bf16 level (as between a ring step and one big step); the
+                # fp32 statistics (lse) only by summation order
+                assert err < (1e-5 if name == "lse" else 8e-3), (name, n_q, err)  # 8e-3: two bf16 ulps
