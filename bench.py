@@ -66,7 +66,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-lmhead", action="store_true", help="skip the cfg5 fused LM-head sub-measurement")
-    ap.add_argument("--no-1m", action="store_true", help="skip the 1M-token headline sub-measurement (N >= 4 only)")
+    ap.add_argument("--no-1m", action="store_true", help="skip the 1M-token headline sub-measurement (N >= 2 only)")
     ap.add_argument("--lm-tokens", type=int, default=131072, help="cfg5: tokens per GPU (2^20 over 8 GPUs)")
     ap.add_argument("--lm-vocab", type=int, default=131072)
     ap.add_argument("--lm-dim", type=int, default=4096)
@@ -526,7 +526,7 @@ def run_gpu(args) -> None:
 
     lm = None if args.no_lmhead else run_lmhead(args, dev, world)
     headline = None
-    if world >= 4 and not args.no_1m and args.seq != HEADLINE_SEQ:
+    if world >= 2 and not args.no_1m and args.seq != HEADLINE_SEQ:
         del q, k, v, do, o, lse, dq, dk, dv
         if ring.transport == "ce":
             ring.close()  # collective: frees this run's copy-engine arenas
@@ -608,7 +608,7 @@ HEADLINE_SEQ = 1 << 20
 
 def run_headline_1m(args, dev, world: int, rank: int, steps: int = 2) -> dict:
     """BASELINE's headline configuration itself (cfg3: 1M-token causal, zigzag, 32 heads, d=128,
-    fwd + burst bwd) on the N >= 4 GPUs of this run, as a sub-measurement of the same line: one
+    fwd + burst bwd) on the N >= 2 GPUs of this run, as a sub-measurement of the same line: one
     warm-up step, ``steps`` timed steps (barrier + sync on both sides, CUDA events, max over
     ranks), then the same compute-lane / exchange-alone split as ``ring_overlap``."""
     import torch
