@@ -568,6 +568,9 @@ def run_gpu(args) -> None:
         "config": workload_config(args, world),
         "tflops_per_gpu": value / world,
         "mfu": value / world / DENSE_BF16_PEAK,
+        # the "model-FLOPs" convention 12·d·Hq·P (no S recompute in the backward)
+        "model_flops_tflops_per_gpu": value / world * 12.0 / 14.0,
+        "model_flops_mfu": value / world * 12.0 / 14.0 / DENSE_BF16_PEAK,
         "frac_of_measured_bf16": value / world / float(peaks.get("bf16_tflops", 1670.0)),
         "e2e": e2e,
         "gpu_launches": int(launches),
@@ -588,6 +591,9 @@ def run_gpu(args) -> None:
         },
         "clocks": clk.summary(),
         "ring_bytes_sent_per_step_rank0": ring_bytes,
+        # the reference's element model for the same passes (fabric.py:306-321), per device,
+        # converted at bf16 activations / fp32 gradients: what account_attention_comm counts
+        "ring_reference_model": comm_model(args, world),
         "ring_overlap": overlap,
         "lmhead": lm,
         "e2e_dropin_api": e2e_api,
@@ -687,6 +693,27 @@ def run_headline_1m(args, dev, world: int, rank: int, steps: int = 2) -> dict:
         ring.close()
     torch.cuda.empty_cache()
     return out
+
+
+def comm_model(args, world: int) -> dict | None:
+    """account_attention_comm (fabric.py:306-321) for this run's forward + backward, per device
+    per step: elements and the bytes they mean here (activations bf16, gradient partials fp32;
+    the reference counts G hops, the ring moves G - 1)."""
+    if world < 2:
+        return None
+    from paper_2509_19836_b200.fabric import FORWARD, account_attention_comm
+
+    hd = args.heads * args.head_dim  # the reference is single-head: d -> Hq * d per token
+    fwd = account_attention_comm(FORWARD, args.seq, hd, world) // world
+    bwd = account_attention_comm(args.backward, args.seq, hd, world) // world
+    if args.backward == "burst_backward":  # 3nd + 2n: Q, dO (bf16), dQ (fp32), lse, D (fp32)
+        n = args.seq // world
+        bwd_bytes = 2 * n * hd * 2 + n * hd * 4 + 2 * n * args.heads * 4
+    else:  # 4nd: K, V (bf16), dK, dV (fp32)
+        n = args.seq // world
+        bwd_bytes = 2 * n * hd * 2 + 2 * n * hd * 4
+    return {"elements_per_device_per_step": fwd + bwd, "bytes_per_device_per_step_at_G_hops": (fwd * 2 + bwd_bytes) * world,
+            "how": "fabric.account_attention_comm per pass / G devices; bytes at bf16 activations and fp32 gradients, G hops"}
 
 
 def run_dropin_e2e(args, layout, mask, host, flops_step: float, steps: int = 2) -> dict:
