@@ -186,3 +186,17 @@ def test_lmhead_models():
         assert L.tile_working_set(rec["n"], rec["v"], rec["d"], cfg) == rec["working_set"]
     with pytest.raises(ValueError):
         L.FusionConfig(0, 4)
+
+
+@pytest.mark.parametrize("kind,n,g,bl", [("contiguous", 64, 4, None), ("zigzag", 64, 4, None), ("zigzag", 64, 1, None),
+                                         ("striped", 64, 4, None), ("block_striped", 64, 2, 8)])
+def test_shard_rows_numpy_equals_the_reference_gather(kind, n, g, bl):
+    """shard_rows on NumPy (distributed.py:118-119): block copies per run of consecutive ids must
+    give exactly x[ids - 1], as new arrays (the reference's fancy index never aliases)."""
+    from paper_2509_19836_b200.distributed import shard_rows
+
+    layout = P.ShardLayout(kind, n, g, bl)
+    for x in (np.random.default_rng(1).standard_normal((n, 3, 5)), np.arange(n * 2, dtype=np.float32).reshape(n, 2)):
+        for ids, part in zip(P.shard_token_arrays(layout), shard_rows(layout, x)):
+            assert np.array_equal(part, x[np.asarray(ids) - 1]) and part.dtype == x.dtype
+            assert not np.shares_memory(part, x)
