@@ -11,7 +11,7 @@ buf = np.zeros(4096, dtype=np.int64)
 N.check(N.load().bb_debug_probe(buf.ctypes.data, 4096))
 t = buf[512:1024].reshape(16, 32)
 base = t[t > 0].min()
-names = {20: "s0:exp", 21: "s0:fenced", 22: "s0:max", 23: "s0:ldS", 28: "s1:exp", 29: "s1:fenced", 30: "s1:max", 31: "s1:ldS", 0: "ld:K?", 1: "ld:K", 2: "ld:V?", 3: "ld:V", 4: "m:K?", 5: "m:K", 6: "m:P0?", 7: "m:P0", 8: "m:P1?", 9: "m:P1",
+names = {20: "s0:exp", 21: "s0:stw", 22: "s0:bits", 23: "s0:ldS", 28: "s1:exp", 29: "s1:stw", 30: "s1:bits", 31: "s1:ldS", 0: "ld:K?", 1: "ld:K", 2: "ld:V?", 3: "ld:V", 4: "m:K?", 5: "m:K", 6: "m:P0?", 7: "m:P0", 8: "m:P1?", 9: "m:P1",
          16: "s0:S?", 17: "s0:S", 18: "s0:pv", 19: "s0:P", 24: "s1:S?", 25: "s1:S", 26: "s1:pv", 27: "s1:P"}
 for it in range(16):
     print(it, " ".join(f"{names[s]}={t[it, s]-base}" for s in sorted(names) if t[it, s] > 0))
