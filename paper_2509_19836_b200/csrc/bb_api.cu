@@ -89,8 +89,8 @@ long long* debug_probe_buffer() {
   if (!checked) {
     checked = true;
     const char* e = getenv("BB_PROBE");
-    if (e && *e == '1' && cudaMalloc(&buf, 4096 * sizeof(long long)) == cudaSuccess)
-      cudaMemset(buf, 0, 4096 * sizeof(long long));
+    if (e && *e == '1' && cudaMalloc(&buf, kProbeEntries * sizeof(long long)) == cudaSuccess)
+      cudaMemset(buf, 0, kProbeEntries * sizeof(long long));
   }
   return buf;
 }
@@ -211,7 +211,7 @@ const char* bb_last_error(void) { return g_err; }
 int bb_debug_probe(int64_t* host_out, int32_t n) {
   long long* buf = debug_probe_buffer();
   if (!buf) return set_error(BB_ERR_UNSUPPORTED, "set BB_PROBE=1 before the first launch");
-  if (n > 4096) n = 4096;
+  if (n > kProbeEntries) n = kProbeEntries;
   return check_cuda(cudaMemcpy(host_out, buf, n * sizeof(long long), cudaMemcpyDeviceToHost), "probe copy");
 }
 int32_t bb_abi_version(void) { return 1; }

@@ -77,7 +77,26 @@ struct FwdParams {
 #define FWD_PROBE(idx, slot) \
   do {                 \
   } while (0)
+#define FWD_CTA_MARK(k) \
+  do {                  \
+  } while (0)
 #else
+// per-CTA timeline: SM id and globaltimer (ns) at entry / prologue done / epilogue / exit
+#define FWD_CTA_MARK(k)                                                                                   \
+  do {                                                                                                    \
+    const int64_t cta_ = static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x;                        \
+    if (p.probe && 4096 + cta_ * 8 + 7 < kProbeEntries) {                                                  \
+      unsigned long long t_;                                                                              \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                              \
+      unsigned smid_;                                                                                     \
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));                                                  \
+      p.probe[4096 + cta_ * 8 + 1 + (k)] = static_cast<long long>(t_);                                     \
+      if ((k) == 0) p.probe[4096 + cta_ * 8] = smid_;                                                      \
+    }                                                                                                     \
+  } while (0)
+#ifndef BB_PROBE_TAIL
+#define BB_PROBE_TAIL 0  // 1: softmax probes index the last 16 key tiles (j_hi - 1 - j) instead of the first
+#endif
 #define FWD_PROBE(idx, slot)                                                                         \
   do {                                                                                               \
     if (p.probe && blockIdx.x == 0 && blockIdx.y == 0 && (idx) < 16) p.probe[512 + (idx) * 32 + (slot)] = clock64(); \
@@ -101,6 +120,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023) != 0) __trap();
 
+  if (threadIdx.x == 0) FWD_CTA_MARK(0);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* q_full = bars + 0;
   uint64_t* kv_full = bars + 1;                      // [KV_SLOTS]
@@ -154,6 +174,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) FWD_CTA_MARK(1);
 
   if (warp < 4) {
     setmaxnreg_dec<REGS_CTRL>();
@@ -293,14 +314,14 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         cls = cls_next;
         continue;
       }
-      if (row == 0) FWD_PROBE(t, 16 + 8 * q);
+      if (row == 0) FWD_PROBE(BB_PROBE_TAIL ? static_cast<uint32_t>(j_hi - 1 - j) : t, 16 + 8 * q);
       mbar_wait(&s_full[q], t & 1);
-      if (row == 0) FWD_PROBE(t, 17 + 8 * q);
+      if (row == 0) FWD_PROBE(BB_PROBE_TAIL ? static_cast<uint32_t>(j_hi - 1 - j) : t, 17 + 8 * q);
       tc_fence_after();
       uint4 bits = make_uint4(~0u, ~0u, ~0u, ~0u);
       if (cls == TILE_PARTIAL)
         bits = row_mask_bits(p.layout, p.mask, q_id, row_ok, p.k_device, j * 128, p.n_k, true);
-      if (row == 0) FWD_PROBE(t, 22 + 8 * q);
+      if (row == 0) FWD_PROBE(BB_PROBE_TAIL ? static_cast<uint32_t>(j_hi - 1 - j) : t, 22 + 8 * q);
       float s[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
@@ -311,7 +332,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         for (int c = 0; c < 128; ++c)
           if (!mask_bit(bits, c)) s[c] = -INFINITY;
       }
-      if (row == 0) FWD_PROBE(t, 23 + 8 * q);
+      if (row == 0) FWD_PROBE(BB_PROBE_TAIL ? static_cast<uint32_t>(j_hi - 1 - j) : t, 23 + 8 * q);
       // Row max as an 8-way tree of 3-input maxes (a 128-long dependent chain is ~512+ cycles).
       float mx8[8];
 #pragma unroll
@@ -336,7 +357,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       // MMA order PV(j-1) .. S(j) this has already happened by the time S(j) is ready).
       if (t > 0) {
         mbar_wait(&pv_done[q], (t - 1) & 1);
-        if (row == 0) FWD_PROBE(t, 18 + 8 * q);
+        if (row == 0) FWD_PROBE(BB_PROBE_TAIL ? static_cast<uint32_t>(j_hi - 1 - j) : t, 18 + 8 * q);
         tc_fence_after();
         if (__any_sync(0xffffffff, need)) {
 #pragma unroll 1
@@ -378,12 +399,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       else
         exp_pass(std::false_type{});
       l_run += ((acc4[0].x + acc4[0].y) + (acc4[1].x + acc4[1].y)) + ((acc4[2].x + acc4[2].y) + (acc4[3].x + acc4[3].y));
-      if (row == 0) FWD_PROBE(t, 20 + 8 * q);
+      if (row == 0) FWD_PROBE(BB_PROBE_TAIL ? static_cast<uint32_t>(j_hi - 1 - j) : t, 20 + 8 * q);
       tmem_st_wait();
-      if (row == 0) FWD_PROBE(t, 21 + 8 * q);
+      if (row == 0) FWD_PROBE(BB_PROBE_TAIL ? static_cast<uint32_t>(j_hi - 1 - j) : t, 21 + 8 * q);
       tc_fence_before();
       mbar_arrive(&p_full[q]);
-      if (row == 0) FWD_PROBE(t, 19 + 8 * q);
+      if (row == 0) FWD_PROBE(BB_PROBE_TAIL ? static_cast<uint32_t>(j_hi - 1 - j) : t, 19 + 8 * q);
       ++t;
       cls = cls_next;
     }
@@ -391,6 +412,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     float* o_row = p.o + (qrow * p.hq + head) * static_cast<int64_t>(D);
     uint2* o16_row = (p.o16 && row_ok) ? p.o16 + (qrow * p.hq + head) * static_cast<int64_t>(D / 4) : nullptr;
     bool written = false;
+    if (row == 0) {
+      if (q == 0) FWD_CTA_MARK(2);
+      else FWD_CTA_MARK(4);
+    }
     if (t > 0) {
       mbar_wait(&pv_done[q], (t - 1) & 1);
       tc_fence_after();
@@ -448,9 +473,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     }
   }
 
+  if (warp >= 4 && (warp & 3) == 0 && lane == 0) FWD_CTA_MARK((warp == 4) ? 5 : 6);  // softmax WG done
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc<512>(tmem);
+  if (threadIdx.x == 0) FWD_CTA_MARK(3);
 }
 
 template <int D>

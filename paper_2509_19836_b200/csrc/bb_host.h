@@ -54,6 +54,9 @@ int launch_gemm_bf16(const void* a, const void* b, void* c16, const int64_t* row
 // lse_ld: row length of the lse (and delta) arrays; a.n_q unless bb_api.cu launches a sub-shard
 int launch_attn_fwd(const bb_attn_fwd_args& a, cudaStream_t stream, int64_t lse_ld);
 int launch_attn_bwd(const bb_attn_bwd_args& a, cudaStream_t stream, int64_t lse_ld);
+// diagnostics buffer (BB_PROBE=1): [0, 4096) per-phase clocks of one CTA, then 8 words per CTA
+// (SM id, globaltimer at entry / end of prologue / epilogue start / exit) from 4096 on
+constexpr int kProbeEntries = 65536;
 // largest shard (rows) one launch takes: the kernels' class tables hold 4096 tiles of 128
 constexpr int64_t MAX_SHARD_ROWS = 4096 * 128;
 

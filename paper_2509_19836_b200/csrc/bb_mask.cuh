@@ -205,26 +205,95 @@ __device__ __forceinline__ void active_runs(const LayoutD& L, const MaskD& M, in
   }
 }
 
+// Bits [lo, hi) of a 128-bit row mask (0 <= lo, hi <= 128).
+__device__ __forceinline__ uint4 range_bits(int32_t lo, int32_t hi) {
+  uint32_t w[4];
+#pragma unroll
+  for (int wd = 0; wd < 4; ++wd) {
+    const int32_t a = max(lo - 32 * wd, 0), b = min(hi - 32 * wd, 32);
+    w[wd] = a >= b ? 0u : ((b == 32 ? 0xFFFFFFFFu : ((1u << b) - 1u)) & ~((1u << a) - 1u));
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__device__ __forceinline__ int64_t floor_div(int64_t a, int64_t b) {  // b > 0
+  const int64_t q = a / b;
+  return (a % b != 0 && a < 0) ? q - 1 : q;
+}
+
 // 128-bit row mask of a PARTIAL tile: bit c set iff (this thread's token, the c-th token of
 // the other side's 128-run) is allowed.  fixed_is_query: the thread owns a query row and the
 // run is keys (forward); otherwise the thread owns a key and the run is queries (backward).
 // Entries past other_n (ragged shard end) are masked.
-static __device__ __noinline__ uint4 row_mask_bits(const LayoutD& L, const MaskD& M, int64_t fixed_id,
+//
+// Causal / sliding-window / full masks allow a contiguous interval of the other side's ids,
+// and within a 128-run those ids form at most a few arithmetic runs (consecutive for
+// contiguous / zigzag rows, step G for striped and inside a block_striped block), so the mask
+// is the union of at most a few bit ranges -- no per-element work.  Block-sparse masks (and
+// runs that split into more pieces) take the per-element predicate.
+static __device__ __noinline__ uint4 row_mask_bits(const LayoutD& Lref, const MaskD& Mref, int64_t fixed_id,
                                                    bool fixed_ok, int32_t other_dev, int64_t other0,
                                                    int64_t other_n, bool fixed_is_query) {
+  // The callers pass references into __grid_constant__ kernel parameters, which this
+  // out-of-line function can only read through generic loads: copy them once.
+  const LayoutD L = Lref;
+  const MaskD M = Mref;
+  if (!fixed_ok || other0 >= other_n) return make_uint4(0u, 0u, 0u, 0u);
+  const int32_t n = static_cast<int32_t>(other_n - other0 < 128 ? other_n - other0 : 128);
+  if (M.kind != MASK_BLOCK) {
+    // interval [vlo, vhi] of the other side's ids that the fixed token may pair with
+    int64_t vlo = INT64_MIN / 4, vhi = INT64_MAX / 4;
+    if (M.kind == MASK_CAUSAL || M.kind == MASK_WINDOW) {
+      const int64_t w = M.kind == MASK_WINDOW ? M.window : INT64_MAX / 4;
+      if (fixed_is_query) {  // keys k with q - w < k <= q
+        vhi = fixed_id;
+        vlo = fixed_id - w + 1;
+      } else {  // queries q with k <= q < k + w
+        vlo = fixed_id;
+        vhi = fixed_id + w - 1;
+      }
+    }
+    // walk the run's arithmetic segments [c0, c1): id = id0 + step * (c - c0); a zigzag run
+    // splits at the shard's half (row p), a block_striped run at every block (per rows)
+    const int64_t step = (L.kind == LAYOUT_STRIPED || L.kind == LAYOUT_BLOCK_STRIPED) ? L.g : 1;
+    if (L.kind != LAYOUT_BLOCK_STRIPED || L.per >= 32) {
+      uint4 bits = make_uint4(0u, 0u, 0u, 0u);
+      for (int32_t c0 = 0; c0 < n;) {
+        int64_t c1 = n;
+        if (L.kind == LAYOUT_ZIGZAG && other0 + c0 < L.p && other0 + n > L.p) c1 = L.p - other0;
+        if (L.kind == LAYOUT_BLOCK_STRIPED) {
+          const int64_t nxt = ((other0 + c0) / L.per + 1) * L.per - other0;
+          if (nxt < c1) c1 = nxt;
+        }
+        const int64_t id0 = token_id(L, other_dev, other0 + c0);
+        // c in [c0, c1) with vlo <= id0 + step (c - c0) <= vhi
+        const int64_t skip = -floor_div(id0 - vlo, step);  // first c - c0 with id >= vlo
+        const int64_t lo = c0 + (skip > 0 ? skip : 0);
+        const int64_t hi = c0 + floor_div(vhi - id0, step) + 1;
+        const int32_t ra = static_cast<int32_t>(lo < c1 ? lo : c1), rb = static_cast<int32_t>(hi < c1 ? hi : c1);
+        if (ra < rb) {
+          const uint4 r = range_bits(ra, rb);
+          bits.x |= r.x;
+          bits.y |= r.y;
+          bits.z |= r.z;
+          bits.w |= r.w;
+        }
+        c0 = static_cast<int32_t>(c1);
+      }
+      return bits;
+    }
+  }
   uint32_t w[4];
 #pragma unroll
   for (int wd = 0; wd < 4; ++wd) {
     uint32_t bits = 0;
-    if (fixed_ok) {
 #pragma unroll 1
-      for (int b = 0; b < 32; ++b) {
-        const int64_t r = other0 + wd * 32 + b;
-        if (r >= other_n) break;
-        const int64_t id = token_id(L, other_dev, r);
-        const bool ok = fixed_is_query ? pair_allowed(M, fixed_id, id) : pair_allowed(M, id, fixed_id);
-        bits |= static_cast<uint32_t>(ok) << b;
-      }
+    for (int b = 0; b < 32; ++b) {
+      const int64_t r = other0 + wd * 32 + b;
+      if (r >= other_n) break;
+      const int64_t id = token_id(L, other_dev, r);
+      const bool ok = fixed_is_query ? pair_allowed(M, fixed_id, id) : pair_allowed(M, id, fixed_id);
+      bits |= static_cast<uint32_t>(ok) << b;
     }
     w[wd] = bits;
   }

@@ -58,6 +58,26 @@ def main():
     tl = ring.trace_collect()
     torch.cuda.synchronize()
     step_ms = e0.elapsed_time(e1)
+    from paper_2509_19836_b200.partitioning import pair_count_matrix
+
+    counts = pair_count_matrix(layout, M.causal_mask())
+
+    def rate(e, r):  # TFLOP/s of one traced attention launch (labels name the shard pair)
+        import re
+        lab = e.label
+        m = re.match(r"forward q(\d+) x k(\d+)", lab)
+        if m:
+            i, j = int(m.group(1)) - 1, int(m.group(2)) - 1
+            return 4.0 * d * h * counts[i, j] / (e.end - e.start) / 1e12
+        m = re.match(r"dq shard (\d+) on (\d+)", lab)
+        if m:
+            i, j = int(m.group(1)) - 1, int(m.group(2)) - 1
+            return 10.0 * d * h * counts[i, j] / (e.end - e.start) / 1e12
+        m = re.match(r"dq own shard ([AB])", lab)
+        if m:
+            return 10.0 * d * h * counts[r, r] / 2 / (e.end - e.start) / 1e12
+        return None
+
     if rank == 0:
         for r in range(world):
             evs = sorted(tl.device_events(r + 1), key=lambda e: e.start)
@@ -71,7 +91,9 @@ def main():
                     if prev_end is not None and e.start - prev_end > 20e-6:
                         gap = f"   <- compute idle {1e3 * (e.start - prev_end):.3f} ms"
                     prev_end = e.end
-                print(f"  {e.kind:11s} {1e3 * e.start:9.3f} {1e3 * e.end:9.3f} {1e3 * (e.end - e.start):8.3f}  {e.label}{gap}")
+                tf = rate(e, r) if e.kind == "compute" else None
+                tfs = f"  [{tf:.0f} TF/s]" if tf else ""
+                print(f"  {e.kind:11s} {1e3 * e.start:9.3f} {1e3 * e.end:9.3f} {1e3 * (e.end - e.start):8.3f}  {e.label}{tfs}{gap}")
     ring.close()
     dist.destroy_process_group()
 
