@@ -92,7 +92,24 @@ struct BwdParams {
 #define BB_PROBE(slot) \
   do {                 \
   } while (0)
+#define BWD_CTA_MARK(k) \
+  do {                  \
+  } while (0)
 #else
+// per-CTA timeline (tools/cta_timeline.py --kernel bwd): SM id, globaltimer at entry / prologue
+// done / compute loop done / dK-dV stored / exit
+#define BWD_CTA_MARK(k)                                                                                   \
+  do {                                                                                                    \
+    const int64_t cta_ = static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x;                        \
+    if (p.probe && 4096 + cta_ * 8 + 7 < kProbeEntries) {                                                  \
+      unsigned long long t_;                                                                              \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                              \
+      unsigned smid_;                                                                                     \
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));                                                  \
+      p.probe[4096 + cta_ * 8 + 1 + (k)] = static_cast<long long>(t_);                                     \
+      if ((k) == 0) p.probe[4096 + cta_ * 8] = smid_;                                                      \
+    }                                                                                                     \
+  } while (0)
 #define BB_PROBE(slot)                                                                 \
   do {                                                                                 \
     if (p.probe && blockIdx.x == 0 && blockIdx.y == 0 && it < 16) p.probe[it * 32 + (slot)] = clock64(); \
@@ -109,11 +126,13 @@ template <int D>
 __global__ void __launch_bounds__(BWD_THREADS, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                     const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
-                    const __grid_constant__ CUtensorMap tdq, const __grid_constant__ BwdParams p) {
+                    const __grid_constant__ CUtensorMap tdq, const __grid_constant__ CUtensorMap tdk,
+                    const __grid_constant__ CUtensorMap tdv, const __grid_constant__ BwdParams p) {
   using L = BwdSmem<D>;
   constexpr int PANELS = D / 64;
   constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 256 + D;
   extern __shared__ __align__(1024) uint8_t smem[];
+  if (threadIdx.x == 0) BWD_CTA_MARK(0);
   if ((smem_u32(smem) & 1023) != 0) __trap();
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* kv_full = bars + 0;
@@ -151,6 +170,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     tma_prefetch(&tv);
     tma_prefetch(&tdo);
     tma_prefetch(&tdq);
+    tma_prefetch(&tdk);
+    tma_prefetch(&tdv);
     mbar_init(kv_full, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&q_full[s], 1);
@@ -185,6 +206,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) BWD_CTA_MARK(1);
   const uint32_t tmem = *tmem_slot;
 
   // Work items: (query head of the GQA group, query tile) in order, skipping masked tiles.
@@ -518,12 +540,17 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       cls = cls_next;
       ++it;
     }
-    // ---- dK (scaled) and dV accumulate into the resident fp32 buffers
+    // ---- dK (scaled) and dV accumulate into the resident fp32 buffers: staged in shared memory
+    // (Q / dO / dS buffers, free once the last MMA retired) and added by TMA bulk reduce-add, so
+    // the CTA never waits on global loads (a register read-modify-write took ~20-25 us per CTA:
+    // its loads queue behind the other SMs' dQ reduce traffic in L2)
+    if (ct == 0) BWD_CTA_MARK(2);
     if (it > 0) {
       mbar_wait(acc_full, 0);
+      if (ct == 0) BWD_CTA_MARK(5);
       tc_fence_after();
-      float* dk_row = p.dk + (krow * p.hkv + kv_head) * static_cast<int64_t>(D);
-      float* dv_row = p.dv + (krow * p.hkv + kv_head) * static_cast<int64_t>(D);
+      uint8_t* stage_k = smem + L::Q_OFF;   // D/32 chunks of [128 keys x 32] fp32, SWIZZLE_128B
+      uint8_t* stage_v = smem + L::DO_OFF;  // (dO + dS buffers)
 #pragma unroll 1
       for (int ce = g; ce < D / 32; ce += NG) {
         const int dcol = ce * 32;
@@ -531,24 +558,24 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         tmem_ld32(tmem + t_lane + COL_DK + dcol, a);
         tmem_ld32(tmem + t_lane + COL_DV + dcol, b);
         tmem_ld_wait();
-        if (key_ok) {
-          float4* k4 = reinterpret_cast<float4*>(dk_row + dcol);
-          float4* v4 = reinterpret_cast<float4*>(dv_row + dcol);
+        uint8_t* kd = stage_k + ce * 16384 + row * 128;
+        uint8_t* vd = stage_v + ce * 16384 + row * 128;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            float4 x = k4[i], y = v4[i];
-            x.x += a[4 * i] * p.scale;
-            x.y += a[4 * i + 1] * p.scale;
-            x.z += a[4 * i + 2] * p.scale;
-            x.w += a[4 * i + 3] * p.scale;
-            y.x += b[4 * i];
-            y.y += b[4 * i + 1];
-            y.z += b[4 * i + 2];
-            y.w += b[4 * i + 3];
-            k4[i] = x;
-            v4[i] = y;
-          }
+        for (int i = 0; i < 8; ++i) {
+          *reinterpret_cast<float4*>(kd + ((i ^ (row & 7)) << 4)) =
+              make_float4(a[4 * i] * p.scale, a[4 * i + 1] * p.scale, a[4 * i + 2] * p.scale, a[4 * i + 3] * p.scale);
+          *reinterpret_cast<float4*>(vd + ((i ^ (row & 7)) << 4)) = make_float4(b[4 * i], b[4 * i + 1], b[4 * i + 2], b[4 * i + 3]);
         }
+      }
+      fence_async_smem();
+      named_bar_sync(7, NCOMP);
+      if (ct == 0) {  // rows past n_k (a ragged last key tile) fall outside the maps and are dropped
+        for (int ce = 0; ce < D / 32; ++ce) {
+          tma_reduce_add_2d(&tdk, stage_k + ce * 16384, kv_head * D + ce * 32, static_cast<int32_t>(c0));
+          tma_reduce_add_2d(&tdv, stage_v + ce * 16384, kv_head * D + ce * 32, static_cast<int32_t>(c0));
+        }
+        bulk_commit();
+        bulk_wait<0>();
       }
     }
   } else {
@@ -611,21 +638,25 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   }
 
   tc_fence_before();
+  if (warp == 4 && lane == 0) BWD_CTA_MARK(3);  // this compute warp's dK / dV rows stored
   __syncthreads();
   if (warp == 2) tmem_dealloc<512>(tmem);
+  if (threadIdx.x == 0) BWD_CTA_MARK(4);
 }
 
 template <int D>
 int launch_bwd_d(const bb_attn_bwd_args& a, cudaStream_t st, int64_t lse_ld) {
   if ((a.n_q + 127) / 128 > MAX_QT)  // bb_api.cu splits larger shards before they get here
     return set_error(BB_ERR_UNSUPPORTED, "attn_bwd: query shard of %lld rows exceeds %d (raise MAX_QT)", (long long)a.n_q, MAX_QT * 128);
-  CUtensorMap tq, tk, tv, tdo, tdq;
+  CUtensorMap tq, tk, tv, tdo, tdq, tdk, tdv;
   const uint64_t qrow = static_cast<uint64_t>(a.hq) * D * 2, krow = static_cast<uint64_t>(a.hkv) * D * 2;
   if (!make_tmap_bf16_2d(&tq, a.q, static_cast<uint64_t>(a.hq) * D, a.n_q, qrow, 64, 128) ||
       !make_tmap_bf16_2d(&tdo, a.dout, static_cast<uint64_t>(a.hq) * D, a.n_q, qrow, 64, 128) ||
       !make_tmap_bf16_2d(&tk, a.k, static_cast<uint64_t>(a.hkv) * D, a.n_k, krow, 64, 128) ||
       !make_tmap_bf16_2d(&tv, a.v, static_cast<uint64_t>(a.hkv) * D, a.n_k, krow, 64, 128) ||
-      !make_tmap_2d(&tdq, a.dq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, static_cast<uint64_t>(a.hq) * D, a.n_q, qrow * 2, 32, 128))
+      !make_tmap_2d(&tdq, a.dq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, static_cast<uint64_t>(a.hq) * D, a.n_q, qrow * 2, 32, 128) ||
+      !make_tmap_2d(&tdk, a.dk, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, static_cast<uint64_t>(a.hkv) * D, a.n_k, krow * 2, 32, 128) ||
+      !make_tmap_2d(&tdv, a.dv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, static_cast<uint64_t>(a.hkv) * D, a.n_k, krow * 2, 32, 128))
     return BB_ERR_CUDA;
   BwdParams p{};
   p.lse = a.lse;
@@ -659,7 +690,7 @@ int launch_bwd_d(const bb_attn_bwd_args& a, cudaStream_t st, int64_t lse_ld) {
   }
   const unsigned n_kt = static_cast<unsigned>((a.n_k + 127) / 128);
   dim3 grid(n_kt, n_heads);
-  kern<<<grid, BWD_THREADS, BwdSmem<D>::BYTES, st>>>(tq, tk, tv, tdo, tdq, p);
+  kern<<<grid, BWD_THREADS, BwdSmem<D>::BYTES, st>>>(tq, tk, tv, tdo, tdq, tdk, tdv, p);
   return check_launch("attn_bwd_kernel");
 }
 

@@ -444,17 +444,21 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         tmem_ld32(tmem + t_lane + (256u + q * D) + c * 32, o);
         tmem_ld_wait();
         if (write) {
-          float4* dst = reinterpret_cast<float4*>(o_row + c * 32);
+          float4* __restrict__ dst = reinterpret_cast<float4*>(o_row + c * 32);
+          // the previous O (ring merge) is loaded whole before any store: interleaved, each load
+          // waited a memory round trip behind the previous (possibly aliasing) store
+          float4 prev[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) prev[i] = w_old != 0.f ? dst[i] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             float4 r = make_float4(o[4 * i] * w_step, o[4 * i + 1] * w_step, o[4 * i + 2] * w_step,
                                    o[4 * i + 3] * w_step);
             if (w_old != 0.f) {
-              const float4 prev = dst[i];
-              r.x += w_old * prev.x;
-              r.y += w_old * prev.y;
-              r.z += w_old * prev.z;
-              r.w += w_old * prev.w;
+              r.x += w_old * prev[i].x;
+              r.y += w_old * prev[i].y;
+              r.z += w_old * prev[i].z;
+              r.w += w_old * prev[i].w;
             }
             dst[i] = r;
             if (o16_row) o16_row[c * 8 + i] = make_uint2(pack_bf16(r.x, r.y), pack_bf16(r.z, r.w));

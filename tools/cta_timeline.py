@@ -23,6 +23,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=16384)
 ap.add_argument("--heads", type=int, default=32)
 ap.add_argument("--mask", default="causal")
+ap.add_argument("--kernel", default="fwd", choices=["fwd", "bwd"])
 args = ap.parse_args()
 dev = torch.device("cuda")
 n, h, d = args.n, args.heads, 128
@@ -36,28 +37,45 @@ for _ in range(2):
     lse.fill_(float("-inf"))
     K.attn_fwd_step(q, k, v, o, lse, layout, dm, 1, 1, 1 / math.sqrt(d))
 torch.cuda.synchronize()
+if args.kernel == "bwd":
+    do = (torch.rand(n, h, d, device=dev) * 2 - 1).to(torch.bfloat16)
+    delta = torch.empty(h, n, device=dev)
+    dq, dk, dv = (torch.zeros(n, h, d, device=dev) for _ in range(3))
+    K.bwd_preprocess(do, o, delta)
+    for _ in range(2):
+        K.attn_bwd_step(q, k, v, do, lse, delta, dq, dk, dv, layout, dm, 1, 1, 1 / math.sqrt(d))
+    torch.cuda.synchronize()
 buf = np.zeros(65536, dtype=np.int64)
 N.check(N.load().bb_debug_probe(buf.ctypes.data, 65536))
-ctas = (n + 255) // 256 * h
+ctas = ((n + 255) // 256 if args.kernel == "fwd" else (n + 127) // 128) * h
 ctas = min(ctas, (65536 - 4096) // 8)
 rec = buf[4096: 4096 + ctas * 8].reshape(ctas, 8)
 rec = rec[rec[:, 1] > 0]
-sm, t0, t1, t2, t3, t4, t5, t6 = (rec[:, i] for i in range(8))
-base = t0.min()
-print(f"{len(rec)} CTAs on {len(set(sm.tolist()))} SMs, kernel span {(t3.max() - base) / 1e3:.1f} us")
-print(f"prologue  mean {np.mean(t1 - t0) / 1e3:.2f} us  max {np.max(t1 - t0) / 1e3:.2f}")
-print(f"main      mean {np.mean(t2 - t1) / 1e3:.2f} us")
-print(f"epilogue  mean {np.mean(t3 - t2) / 1e3:.2f} us  max {np.max(t3 - t2) / 1e3:.2f}")
-print(f"  query tile 1 loop ends after tile 0's by {np.mean(t4 - t2) / 1e3:.2f} us (mean)")
-print(f"  tile 0 epilogue {np.mean(t5 - t2) / 1e3:.2f} us, tile 1 epilogue {np.mean(t6 - t4) / 1e3:.2f} us, "
-      f"exit after the later one {np.mean(t3 - np.maximum(t5, t6)) / 1e3:.2f} us")
+base = rec[:, 1].min()
+sm = rec[:, 0]
+if args.kernel == "fwd":
+    t0, t1, t2, t3, t4, t5, t6 = (rec[:, i] for i in range(1, 8))
+    print(f"{len(rec)} CTAs on {len(set(sm.tolist()))} SMs, kernel span {(t3.max() - base) / 1e3:.1f} us")
+    print(f"prologue  mean {np.mean(t1 - t0) / 1e3:.2f} us  max {np.max(t1 - t0) / 1e3:.2f}")
+    print(f"main      mean {np.mean(t2 - t1) / 1e3:.2f} us")
+    print(f"epilogue  mean {np.mean(t3 - t2) / 1e3:.2f} us  max {np.max(t3 - t2) / 1e3:.2f}")
+    print(f"  query tile 1 loop ends after tile 0's by {np.mean(t4 - t2) / 1e3:.2f} us (mean)")
+    end = t3
+else:
+    t0, t1, t2, t3, t4, t5 = (rec[:, i] for i in range(1, 7))
+    print(f"{len(rec)} CTAs on {len(set(sm.tolist()))} SMs, kernel span {(t4.max() - base) / 1e3:.1f} us")
+    print(f"prologue  mean {np.mean(t1 - t0) / 1e3:.2f} us  max {np.max(t1 - t0) / 1e3:.2f}")
+    print(f"main      mean {np.mean(t2 - t1) / 1e3:.2f} us")
+    print(f"dK/dV     mean {np.mean(t3 - t2) / 1e3:.2f} us (acc_full wait {np.mean(t5 - t2) / 1e3:.2f} us, "
+          f"stores {np.mean(t3 - t5) / 1e3:.2f} us);  then exit {np.mean(t4 - t3) / 1e3:.2f} us")
+    end = t4
 gaps, busy, ends = [], [], []
-for s in set(sm.tolist()):
-    idx = np.argsort(t0[sm == s])
-    a, b = t0[sm == s][idx], t3[sm == s][idx]
+for s_ in set(sm.tolist()):
+    idx = np.argsort(t0[sm == s_])
+    a, b = t0[sm == s_][idx], end[sm == s_][idx]
     gaps.extend((a[1:] - b[:-1]).tolist())
     busy.append(int(np.sum(b - a)))
     ends.append(int(b[-1] - base))
 print(f"gap between CTAs on an SM: mean {np.mean(gaps) / 1e3:.2f} us  max {np.max(gaps) / 1e3:.2f}")
-print(f"SM busy fraction: {np.sum(busy) / (len(busy) * (t3.max() - base)):.3f}; last CTA end spread "
+print(f"SM busy fraction: {np.sum(busy) / (len(busy) * (end.max() - base)):.3f}; last CTA end spread "
       f"{(max(ends) - min(ends)) / 1e3:.1f} us")
