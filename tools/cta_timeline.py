@@ -24,6 +24,7 @@ ap.add_argument("--n", type=int, default=16384)
 ap.add_argument("--heads", type=int, default=32)
 ap.add_argument("--mask", default="causal")
 ap.add_argument("--kernel", default="fwd", choices=["fwd", "bwd"])
+ap.add_argument("--merge", action="store_true", help="fwd: time a second step that merges into the first's (O, lse)")
 args = ap.parse_args()
 dev = torch.device("cuda")
 n, h, d = args.n, args.heads, 128
@@ -36,6 +37,8 @@ for _ in range(2):
     o.zero_()
     lse.fill_(float("-inf"))
     K.attn_fwd_step(q, k, v, o, lse, layout, dm, 1, 1, 1 / math.sqrt(d))
+if args.merge and args.kernel == "fwd":
+    K.attn_fwd_step(q, k, v, o, lse, layout, dm, 1, 1, 1 / math.sqrt(d))  # w_old != 0 everywhere
 torch.cuda.synchronize()
 if args.kernel == "bwd":
     do = (torch.rand(n, h, d, device=dev) * 2 - 1).to(torch.bfloat16)
