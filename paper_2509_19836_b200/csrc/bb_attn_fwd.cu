@@ -301,10 +301,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     const int64_t q_id = row_ok ? token_id(p.layout, p.q_device, qrow) : 0;
     const uint32_t t_lane = (quad * 32) << 16;
     const float sl2 = p.scale_log2;
-    // The running lse this step merges into is read now (only this CTA writes these rows), so
-    // the epilogue does not start with a memory round trip; when it is finite (a ring step after
-    // the first) the previous O rows are prefetched into L2 a few key tiles before the end.
-    const float lse_prev0 = row_ok ? p.lse[static_cast<int64_t>(head) * p.lse_ld + qrow] : -INFINITY;
 
     float m_run = -INFINITY, l_run = 0.f;
     uint32_t t = 0;
@@ -313,11 +309,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     int64_t j = j_lo;
     int32_t cls = j < j_hi ? static_cast<int32_t>((tile_nib(j) >> (2 * q)) & 3u) : TILE_SKIP;
     for (; j < j_hi; ++j) {
-      if (j == max(j_lo, j_hi - 4) && lse_prev0 != -INFINITY) {
-        const float* o_prev = p.o + (qrow * p.hq + head) * static_cast<int64_t>(D);
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c) prefetch_l2(o_prev + c * 32);
-      }
       const int32_t cls_next = j + 1 < j_hi ? static_cast<int32_t>((tile_nib(j + 1) >> (2 * q)) & 3u) : TILE_SKIP;
       if (cls == TILE_SKIP) {
         cls = cls_next;
@@ -435,7 +426,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       written = write;
       float* lse_ptr = p.lse + static_cast<int64_t>(head) * p.lse_ld + qrow;
       if (write) {
-        const float lse_prev = lse_prev0;
+        const float lse_prev = *lse_ptr;
         if (lse_prev == -INFINITY) {
           lse_new = lse_step;
           w_step = 1.f / l_run;
