@@ -159,6 +159,15 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     active_runs(p.layout, p.mask, token_id(p.layout, p.k_device, c0),
                 token_id(p.layout, p.k_device, min(c0 + 128, p.n_k) - 1), p.q_device, p.n_q, false, q_lo, q_hi);
   const uint32_t nr = static_cast<uint32_t>(q_hi - q_lo);
+  // Each CTA walks its query tiles starting at a different one (rotation by its key tile): in a
+  // fully visible block every CTA's range is the same, and in lockstep the ~148 resident CTAs
+  // reduce-added into the same dQ tile at once (a 1M-token 2-GPU remote step ran at 795 TF/s
+  // against 1015 for the causal own step, whose CTAs start at their own diagonal).
+  const uint32_t rot = nr ? static_cast<uint32_t>(blockIdx.x) % nr : 0u;
+  auto phys = [&](uint32_t li) {  // logical item index -> position in [q_lo, q_hi)
+    const uint32_t x = li + rot;
+    return x >= nr ? x - nr : x;
+  };
   // Work item w packs (head-in-group << 16 | query-tile index): no divisions on the roles'
   // per-tile path (a u32 div/mod is a ~100-cycle dependent chain).  n_work = end sentinel.
   const int64_t n_work = static_cast<int64_t>(group) << 16;
@@ -217,11 +226,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     for (;;) {
       if ((w & 0xFFFF) >= nr) w = ((w >> 16) + 1) << 16;
       if (w >= n_work) return n_work;
-      if (tile_cls(static_cast<uint32_t>(q_lo) + static_cast<uint32_t>(w & 0xFFFF)) != TILE_SKIP) return w;
+      if (tile_cls(static_cast<uint32_t>(q_lo) + phys(static_cast<uint32_t>(w & 0xFFFF))) != TILE_SKIP) return w;
       ++w;
     }
   };
-  auto item_qt = [&](int64_t w) { return static_cast<uint32_t>(q_lo) + static_cast<uint32_t>(w & 0xFFFF); };
+  auto item_qt = [&](int64_t w) { return static_cast<uint32_t>(q_lo) + phys(static_cast<uint32_t>(w & 0xFFFF)); };
   auto item_head = [&](int64_t w) { return kv_head * group + static_cast<int>(w >> 16); };
 
   if (warp < 4) {
@@ -437,8 +446,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 32; i += 4)
           *reinterpret_cast<float4*>(&l2[c2][i]) = *reinterpret_cast<const float4*>(&lse2[(g * CH + c2) * 32 + i]);
-      const uint32_t nxt = item_qt(w) + 1 - static_cast<uint32_t>(q_lo);  // next tile's class-table index
-      const uint32_t cls_byte = nxt < nr ? cls_tab[nxt >> 2] : 0u;
+      const bool same_head = (static_cast<uint32_t>(w & 0xFFFF) + 1) < nr;  // next item: same head, next tile
+      const uint32_t nxt = phys(static_cast<uint32_t>(w & 0xFFFF) + 1);      // its class-table index
+      const uint32_t cls_byte = same_head ? cls_tab[nxt >> 2] : 0u;
       uint32_t pk[CH][16];
       float dl[CH][32];
       auto load_dl = [&]() {
@@ -487,7 +497,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       int64_t w_next;
       int32_t cls_next;
       const int32_t c_adj = static_cast<int32_t>((cls_byte >> ((nxt & 3) * 2)) & 3);
-      if (nxt < nr && c_adj != TILE_SKIP) {
+      if (same_head && c_adj != TILE_SKIP) {
         w_next = w + 1;
         cls_next = c_adj;
       } else {
