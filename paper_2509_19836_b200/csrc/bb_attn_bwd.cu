@@ -313,6 +313,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 
       mbar_wait(kv_full, 0);
       int64_t w = next_active(0);
+      // The item after next is looked up while the issuer waits on do_full / dq_free (the
+      // class-table walk is shared loads, which queue behind the SS MMAs' operand reads), not
+      // at the loop top between dP(t+1) and dV(t+1).
+      int64_t wn = w < n_work ? next_active(w + 1) : n_work;
       if (w < n_work) {
         mbar_wait(&q_full[0], 0);
         tc_fence_after();
@@ -322,7 +326,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         issue_dp();
       }
       for (uint32_t it = 0; w < n_work; ++it) {
-        const int64_t wn = next_active(w + 1);
         const uint32_t qs = it & 1;
         const uint32_t q_base = smem_u32(smem + L::Q_OFF + qs * L::TILE);
         if (lane == 0) BB_PROBE(4);
@@ -362,6 +365,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         }
         __syncwarp();
         if (lane == 0) BB_PROBE(10);
+        const int64_t wnn = wn < n_work ? next_active(wn + 1) : n_work;
         if (wn < n_work) {
           mbar_wait(do_full, (it + 1) & 1);
           if (lane == 0) BB_PROBE(6);
@@ -372,6 +376,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           if (lane == 0) BB_PROBE(11);
         }
         w = wn;
+        wn = wnn;
       }
       if (elect_one()) umma_commit(acc_full);
       __syncwarp();
