@@ -721,6 +721,7 @@ def run_dropin_e2e(args, layout, mask, host, flops_step: float, steps: int = 2) 
     NumPy arrays in -> make_device_states -> distributed_forward -> burst_backward(shard_rows(dO))
     -> backward_grads -> float64 NumPy gradients out, every byte of it inside the timed region
     (pageable host memory, as a NumPy caller has it).  Wall clock around synchronised steps."""
+    import numpy as np
     import torch
 
     import paper_2509_19836_b200 as bb
@@ -746,7 +747,9 @@ def run_dropin_e2e(args, layout, mask, host, flops_step: float, steps: int = 2) 
         "unit": "TFLOPS",
         "ms_per_step": t * 1e3,
         "steps": steps,
-        "h2d_bytes_per_step": sum(x.nbytes for x in host),
+        # float32 arrays of an unpadded head dim cross PCIe as bf16 (host cast, distributed._upload)
+        "h2d_bytes_per_step": sum(x.size * 2 if x.dtype == np.float32 and x.shape[-1] in (64, 128) else x.nbytes
+                                  for x in host),
         "d2h_bytes_per_step": sum(x.size * 4 for x in (g[0].dq, g[0].dk, g[0].dv)),
         "output_dtype": str(g[0].dq.dtype),
         "how": "NumPy float32 [N, H, d] in, float64 NumPy dQ/dK/dV out through make_device_states, distributed_forward, "

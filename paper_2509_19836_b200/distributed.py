@@ -119,6 +119,16 @@ def _physical_devices(g: int, devices) -> list[torch.device]:
     return [torch.device("cuda", i % n) for i in range(g)]
 
 
+def _upload(a: np.ndarray, dev: torch.device) -> torch.Tensor:
+    """NumPy [.., d] -> CUDA tensor through pinned staging.  float32 arrays whose d needs no
+    padding are cast to the kernels' bf16 on the host (round to nearest even, the same value
+    the device cast gives), halving the bytes on PCIe; anything else goes up as float32 and
+    is cast (and padded) on the device, as before."""
+    if a.dtype == np.float32 and a.shape[-1] == K.padded_head_dim(a.shape[-1]):
+        return hostio.to_device(a, dev, torch.bfloat16)
+    return hostio.to_device(a, dev)
+
+
 def _as_global(x, name: str, dev: torch.device) -> tuple[torch.Tensor, bool]:
     """Caller array -> CUDA tensor [N, H, d] (fp32 or bf16), plus 'was 2-D'."""
     if isinstance(x, np.ndarray) or not isinstance(x, torch.Tensor):
@@ -128,7 +138,7 @@ def _as_global(x, name: str, dev: torch.device) -> tuple[torch.Tensor, bool]:
             a = a[:, None, :]
         if a.ndim != 3:
             raise ValueError(f"{name} must be [N, d] or [N, H, d], got shape {tuple(a.shape)}")
-        return hostio.to_device(a, dev), two_d  # float32 on the device, via pinned staging
+        return _upload(a, dev), two_d  # via pinned staging
     t = x
     two_d = t.ndim == 2
     if two_d:
@@ -406,7 +416,7 @@ def _do_shards(states: list[DeviceState], do_shards) -> list[torch.Tensor]:
         if t.shape[0] != st.q.shape[0] or t.shape[1] != st.q.shape[1]:
             raise ValueError(f"dO shard for device {st.index} has shape {tuple(t.shape)}, expected {tuple(st.q.shape[:2])} x d")
         if host:
-            t = hostio.to_device(t, st.device)
+            t = _upload(t, st.device)
         elif t.dtype not in (torch.bfloat16, torch.float32):
             t = t.to(torch.float32)
         out.append(_to_kernel_bf16(t.to(st.device), st.q.shape[2]))

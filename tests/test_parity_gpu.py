@@ -126,6 +126,31 @@ def test_golden_fixtures(cuda):
     assert checked == len(meta()["dist"])
 
 
+@pytest.mark.parametrize("d", [128, 100, 64])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_numpy_upload_rounds_like_the_device_cast(cuda, d, dtype):
+    """make_device_states / burst_backward take NumPy float32 of an unpadded head dim as bf16
+    cast on the host (half the PCIe bytes); every path must hold the bits a float32 tensor
+    cast to bf16 on the device holds (zero-padded to the kernels' head dim)."""
+    n, h, g = 512, 2, 2
+    rng = np.random.default_rng(d)
+    x = (rng.standard_normal((n, h, d)) * np.float64(3.0) ** rng.integers(-20, 20, (n, h, d))).astype(dtype)
+    layout = bb.ShardLayout("zigzag", n, g)
+    st = bb.make_device_states(layout, x, x, x)
+    d_pad = 64 if d <= 64 else 128
+    ref = torch.zeros(n, h, d_pad, dtype=torch.bfloat16)
+    ref[..., :d] = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16)
+    ids = bb.shard_token_arrays(layout)
+    for s_, rows in zip(st, ids):
+        want = ref[torch.from_numpy(rows - 1)]
+        for t in (s_.q, s_.k, s_.v):
+            assert torch.equal(t.cpu().view(torch.int16), want.view(torch.int16))
+    from paper_2509_19836_b200.distributed import _do_shards
+
+    for t, s_, rows in zip(_do_shards(st, bb.shard_rows(layout, x)), st, ids):
+        assert torch.equal(t.cpu().view(torch.int16), ref[torch.from_numpy(rows - 1)].view(torch.int16))
+
+
 def test_reference_style_api_2d(cuda):
     """2-D [N, d] arrays in, reference-shaped NumPy out (forward_results / backward_grads)."""
     n, d, g = 64, 16, 4
