@@ -92,12 +92,13 @@ class DeviceState:
     def device(self) -> torch.device:
         return self.q.device
 
-    def result(self, name: str) -> np.ndarray:
-        """A field as float64 NumPy in the caller's convention ([n, d] for 2-D inputs, lse [n])."""
+    def result(self, name: str, out: np.ndarray | None = None) -> np.ndarray:
+        """A field as float64 NumPy in the caller's convention ([n, d] for 2-D inputs, lse [n]);
+        ``out``: a preallocated float64 array of the field's full shape (``hostio.empty_f64``)."""
         t = getattr(self, name)
         if t is None:
             raise RuntimeError(f"{name} has not been computed")
-        a = hostio.to_host_f64(t)  # pinned staging + threaded host cast
+        a = hostio.to_host_f64(t, out)  # pinned staging + threaded host cast
         if name in ("lse", "d_vec"):
             return a[0] if self.single_head else a
         a = a[..., : self.head_dim]
@@ -533,7 +534,16 @@ def ring_backward(
 
 
 def backward_grads(states: list[DeviceState]) -> list[AttentionGrads]:
-    return [AttentionGrads(dq=st.result("dq"), dk=st.result("dk"), dv=st.result("dv")) for st in states]
+    # The backward kernels are still running when a caller gets here (nothing in the passes
+    # waits for them): allocate and page in every float64 result first, so that host work
+    # overlaps the GPU and the copies afterwards write to resident pages.
+    names = ("dq", "dk", "dv")
+    for st in states:
+        for name in names:
+            if getattr(st, name) is None:
+                raise RuntimeError(f"{name} has not been computed")
+    outs = [{name: hostio.empty_f64(getattr(st, name)) for name in names} for st in states]
+    return [AttentionGrads(**{name: st.result(name, o[name]) for name in names}) for st, o in zip(states, outs)]
 
 
 @dataclass

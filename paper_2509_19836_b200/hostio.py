@@ -27,15 +27,29 @@ def _stage(dev: torch.device):
     return s
 
 
-def to_host_f64(t: torch.Tensor) -> np.ndarray:
-    """float64 NumPy copy of a CUDA float tensor (any float dtype, made contiguous first)."""
+def empty_f64(t: torch.Tensor) -> np.ndarray:
+    """A float64 NumPy array shaped like ``t`` whose pages are already resident: written once
+    (zeros, torch's thread pool) so the copy into it later does not stop on first-touch page
+    faults.  Called while the GPU still runs the kernels that produce ``t``, this host work
+    overlaps them (``backward_grads``)."""
+    out = np.empty(tuple(t.shape), dtype=np.float64)
+    torch.from_numpy(out).zero_()
+    return out
+
+
+def to_host_f64(t: torch.Tensor, out: np.ndarray | None = None) -> np.ndarray:
+    """float64 NumPy copy of a CUDA float tensor (any float dtype, made contiguous first),
+    into ``out`` if given (a C-contiguous float64 array of ``t``'s shape)."""
     if not t.is_cuda:
         return t.detach().double().numpy()
     src = t.detach()
     if src.dtype != torch.float32:
         src = src.float()
     src = src.contiguous().reshape(-1)
-    out = np.empty(tuple(t.shape), dtype=np.float64)
+    if out is None:
+        out = np.empty(tuple(t.shape), dtype=np.float64)
+    elif out.shape != tuple(t.shape) or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a C-contiguous float64 array of shape {tuple(t.shape)}")
     dst = torch.from_numpy(out).reshape(-1)
     n = src.numel()
     if n == 0:
