@@ -40,16 +40,20 @@ def empty_f64(t: torch.Tensor) -> np.ndarray:
 def to_host_f64(t: torch.Tensor, out: np.ndarray | None = None) -> np.ndarray:
     """float64 NumPy copy of a CUDA float tensor (any float dtype, made contiguous first),
     into ``out`` if given (a C-contiguous float64 array of ``t``'s shape)."""
+    if out is not None and (out.shape != tuple(t.shape) or out.dtype != np.float64 or not out.flags.c_contiguous):
+        raise ValueError(f"out must be a C-contiguous float64 array of shape {tuple(t.shape)}")
     if not t.is_cuda:
-        return t.detach().double().numpy()
+        a = t.detach().double().numpy()
+        if out is None:
+            return a
+        out[...] = a
+        return out
     src = t.detach()
     if src.dtype != torch.float32:
         src = src.float()
     src = src.contiguous().reshape(-1)
     if out is None:
         out = np.empty(tuple(t.shape), dtype=np.float64)
-    elif out.shape != tuple(t.shape) or out.dtype != np.float64 or not out.flags.c_contiguous:
-        raise ValueError(f"out must be a C-contiguous float64 array of shape {tuple(t.shape)}")
     dst = torch.from_numpy(out).reshape(-1)
     n = src.numel()
     if n == 0:

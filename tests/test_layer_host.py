@@ -49,3 +49,22 @@ def test_attention_backward_checks_shapes_before_the_device():
         attention_backward(q, k, v, o, np.zeros(5), do, causal_mask())
     with pytest.raises(ValueError, match="block_mask must be 2x2"):  # mask smaller than the sequence
         attention_backward(q, k, v, o, lse, do, block_sparse_mask(np.ones((1, 1)), 4))
+
+
+def test_hostio_out_arrays():
+    """to_host_f64 fills a preallocated float64 result (backward_grads pages it in early) and
+    rejects one of the wrong shape / dtype / layout."""
+    import numpy as np
+    import pytest
+    import torch
+
+    from paper_2509_19836_b200 import hostio
+
+    t = torch.arange(24, dtype=torch.float32).reshape(2, 3, 4) / 7
+    out = hostio.empty_f64(t)
+    assert out.shape == (2, 3, 4) and out.dtype == np.float64 and not out.any()
+    res = hostio.to_host_f64(t, out)
+    assert res is out and np.array_equal(out, t.double().numpy())
+    for bad in (np.empty((2, 3, 5)), np.empty((2, 3, 4), dtype=np.float32), np.empty((4, 3, 2)).transpose(2, 1, 0)):
+        with pytest.raises(ValueError):
+            hostio.to_host_f64(t, bad)
