@@ -433,6 +433,10 @@ def run_gpu(args) -> None:
                 "events": len(tl.events), "validated": True, "makespan_ms": tl.makespan * 1e3,
                 "busiest_rank_compute_ms": busiest * 1e3, "sends": len(sends),
                 "send_ms_total_per_rank": sum(e.end - e.start for e in sends) / world * 1e3,
+                # each push's own rate: its channel's payload bytes / its measured duration
+                # (a copy-engine copy over one NVLink path while every SM runs attention kernels)
+                "push_gbs_per_copy": _rate_summary([ring._channels[e.label.split()[0]].payload_bytes / (e.end - e.start) / 1e9
+                                                    for e in sends if e.end > e.start]),
                 "analytic_comm_ms_burst_strategy": analytic_comm_time("burst", link, per_step) * 1e3,
                 "how": "CUDA events around every kernel and push of one step, common origin at a barrier; validate_timeline on the assembled schema",
             }
@@ -714,6 +718,13 @@ def comm_model(args, world: int) -> dict | None:
         bwd_bytes = 2 * n * hd * 2 + 2 * n * hd * 4
     return {"elements_per_device_per_step": fwd + bwd, "bytes_per_device_per_step_at_G_hops": (fwd * 2 + bwd_bytes) * world,
             "how": "fabric.account_attention_comm per pass / G devices; bytes at bf16 activations and fp32 gradients, G hops"}
+
+
+def _rate_summary(xs: list) -> dict | None:
+    if not xs:
+        return None
+    xs = sorted(xs)
+    return {"min": xs[0], "median": xs[len(xs) // 2], "max": xs[-1], "n": len(xs)}
 
 
 def run_dropin_e2e(args, layout, mask, host, flops_step: float, steps: int = 2) -> dict:
