@@ -32,9 +32,9 @@ def main():
     streams = [torch.cuda.Stream(dev) for _ in range(2)]
     out = {}
 
-    def run(kind, both, k):
-        best = 0.0
-        for _ in range(5):
+    def run(kind, both, k, arena_dst=False, pieces=1):
+        rates = []
+        for _ in range(7):
             torch.cuda.synchronize()
             dist.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -43,27 +43,38 @@ def main():
             active = both or rank == 0
             if active:
                 part = n // k
+                mine = ch.base if arena_dst else local.data_ptr()  # pull target: my arena or a torch buffer
                 for i in range(k):
                     s = streams[i]
                     s.wait_event(e0)
                     if kind == "push":  # my buffer -> the peer's arena
                         dst, src = ch.peer_base[peer] + i * part, local.data_ptr() + i * part
                     else:  # the peer's arena -> my buffer
-                        dst, src = local.data_ptr() + i * part, ch.peer_base[peer] + i * part
-                    N.check(lib.bb_copy_async(C.c_void_p(dst), C.c_void_p(src), part, C.c_void_p(s.cuda_stream)))
+                        dst, src = mine + i * part, ch.peer_base[peer] + i * part
+                    piece = part // pieces  # several back-to-back copies on the stream (the ring's per-tensor copies)
+                    for j in range(pieces):
+                        N.check(lib.bb_copy_async(C.c_void_p(dst + j * piece), C.c_void_p(src + j * piece), piece,
+                                                  C.c_void_p(s.cuda_stream)))
                 for s in streams[:k]:
                     cur.wait_stream(s)
             e1.record(cur)
             torch.cuda.synchronize()
             t = torch.tensor([e0.elapsed_time(e1) / 1e3], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            best = max(best, n / float(t.item()) / 1e9)
-        out[f"{kind}_{'bidir' if both else 'unidir'}_{k}streams_GBps_per_direction"] = best
+            rates.append(n / float(t.item()) / 1e9)
+        tag = ("_arena_dst" if arena_dst else "") + (f"_{pieces}pieces" if pieces > 1 else "")
+        rates.sort()
+        out[f"{kind}_{'bidir' if both else 'unidir'}_{k}streams{tag}_GBps_per_direction"] = {
+            "best": rates[-1], "median": rates[len(rates) // 2], "worst": rates[0]}
 
     for kind in ("push", "pull"):
         for both in (False, True):
             for k in (1, 2):
                 run(kind, both, k)
+    for kind in ("push", "pull"):
+        run(kind, True, 1, pieces=2)
+    run("pull", True, 1, arena_dst=True)
+    out["CUDA_DEVICE_MAX_CONNECTIONS"] = os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS")
     if rank == 0:
         print(json.dumps({"ipc_arena_copy_engine": out, "bytes_per_copy": n}), flush=True)
     ch.close()
