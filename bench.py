@@ -270,9 +270,21 @@ def make_mask(args):
     return block_sparse_mask(np.logical_and(band, docs).astype(np.int64), args.block_len)
 
 
+def _config_name(args) -> str:
+    """BASELINE.json config the arguments describe (the default is cfg2)."""
+    kv = args.kv_heads or args.heads
+    if args.seq == 131072 and args.heads == 32 and kv == 32 and args.head_dim == 128 and args.mask == "causal":
+        return "cfg2 LLaMA-7B attention"
+    if args.seq == 524288 and args.heads == 32 and kv == 8 and args.head_dim == 128 and args.mask == "swa_doc":
+        return "cfg4 GQA + SWA + document attention"
+    if args.seq == 1 << 20 and args.mask == "causal":
+        return "cfg3 1M-token causal attention"
+    return "attention (off the BASELINE configs)"
+
+
 def workload_config(args, world: int) -> dict:
     return {
-        "workload": f"cfg2 LLaMA-7B attention: {args.heads} heads (kv {args.kv_heads or args.heads}), d={args.head_dim}, "
+        "workload": f"{_config_name(args)}: {args.heads} heads (kv {args.kv_heads or args.heads}), d={args.head_dim}, "
         f"seq {args.seq} {args.mask}, {args.layout} layout, fwd + {args.backward}, ring {args.topology or f'1x{world}'}",
         "seq_len": args.seq,
         "heads": args.heads,
