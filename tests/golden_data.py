@@ -41,3 +41,17 @@ def unpack_pairs(key: str, g: int, n: int) -> np.ndarray:
     """[G*G, n/G, n/G] bool stack of local pair masks (i-major, j-minor)."""
     size = n // g
     return np.unpackbits(arrays()[key], axis=-1, count=size).astype(bool)
+
+
+def cfg4_golden():
+    """tests/golden/golden_cfg4_fp64.npz (make_cfg4_golden.py: burstsim on a cfg4-shaped case),
+    with the inputs regenerated from their seeds: (arrays, N, G, D, layout block, mask block, Hq)."""
+    from oracle import burst_oracle as O
+
+    A = dict(np.load(GOLDEN / "golden_cfg4_fp64.npz"))
+    n, g, d, lb, mb, _w, _doc, hq = (int(x) for x in A["meta"])
+    A["k"] = O.seeded_random_matrix(n, d, 4001)[:, None]
+    A["v"] = O.seeded_random_matrix(n, d, 4002)[:, None]
+    A["q"] = np.stack([O.seeded_random_matrix(n, d, 4010 + h) for h in range(hq)], axis=1)
+    A["do"] = np.stack([O.seeded_random_matrix(n, d, 4020 + h) for h in range(hq)], axis=1)
+    return A, n, g, d, lb, mb, hq

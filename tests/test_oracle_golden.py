@@ -168,3 +168,41 @@ def test_checkpoint_recompute_exact():
     assert pairs == 16 * 17 // 2  # m(m+1)/2, pkg/tests/test_checkpointing.py:34-61
     for a, b in zip(got, base):
         assert np.max(np.abs(a - b)) < 1e-10
+
+
+@pytest.mark.parametrize("which", ["burst", "ring"])
+def test_cfg4_shaped_case_matches_reference(which):
+    """cfg4's structure scaled down (make_cfg4_golden.py): block_striped over 4 devices, a
+    sliding-window band AND causal documents as one block_sparse mask, two query heads on one
+    K/V head.  The reference ran each query head alone; GQA's dK/dV are their sums."""
+    from golden_data import cfg4_golden
+
+    A, n, g, d, lb, mb, hq = cfg4_golden()
+    res = O.mh_ring_attention(A["q"], A["k"], A["v"], A["do"], ("block_striped", n, g, lb),
+                              ("block_sparse", None, mb, A["block_mask"]), O.ring_visit(1, g), backward=which)
+    for h in range(hq):
+        assert np.max(np.abs(res["o"][:, h] - A[f"o{h}"])) < 1e-12
+        assert np.max(np.abs(res["lse"][h] - A[f"lse{h}"])) < 1e-12
+        assert np.max(np.abs(res["dq"][:, h] - A[f"dq{h}"])) < 1e-12
+    assert np.max(np.abs(res["dk"][:, 0] - (A["dk0"] + A["dk1"]))) < 1e-12
+    assert np.max(np.abs(res["dv"][:, 0] - (A["dv0"] + A["dv1"]))) < 1e-12
+    if which == "ring":  # the reference's K/V-circulating pass (head 0 alone) agrees with its burst pass
+        r0 = O.mh_ring_attention(A["q"][:, :1], A["k"], A["v"], A["do"][:, :1], ("block_striped", n, g, lb),
+                                 ("block_sparse", None, mb, A["block_mask"]), O.ring_visit(1, g), backward="ring")
+        for name in ("dq", "dk", "dv"):
+            assert np.max(np.abs(r0[name][:, 0] - A[f"ring_{name}0"])) < 1e-12
+
+
+def test_cfg4_shaped_mask_is_the_bench_construction():
+    """The golden's block mask (band AND documents, built inside the generator) is what the
+    package's own constructors give: block_mask_from_window AND document_mask (bench.py swa_doc)."""
+    from golden_data import cfg4_golden
+
+    from paper_2509_19836_b200.masks import document_mask
+    from paper_2509_19836_b200.partitioning import block_mask_from_window
+
+    A, n, *_ = cfg4_golden()
+    _, _, _, _, mb, w, doc, _ = (int(x) for x in A["meta"])
+    band = block_mask_from_window(n, mb, w).block_mask
+    docs = document_mask([doc] * (n // doc), mb).block_mask
+    assert np.array_equal(np.logical_and(band, docs).astype(np.int64), A["block_mask"])

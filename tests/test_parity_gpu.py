@@ -151,6 +151,26 @@ def test_numpy_upload_rounds_like_the_device_cast(cuda, d, dtype):
         assert torch.equal(t.cpu().view(torch.int16), ref[torch.from_numpy(rows - 1)].view(torch.int16))
 
 
+@pytest.mark.parametrize("backward", ["burst", "ring"])
+def test_cfg4_shaped_golden(cuda, backward):
+    """cfg4's structure scaled down (tests/golden/make_cfg4_golden.py, burstsim outputs):
+    block_striped over 4 devices, window band AND causal documents as one block_sparse mask,
+    2 query heads on 1 K/V head (GQA pinned as the sum of the reference's per-head runs);
+    unquantised fp64 inputs, the same tolerances as test_golden_fixtures."""
+    from golden_data import cfg4_golden
+
+    A, n, g, d, lb, mb, hq = cfg4_golden()
+    layout = bb.ShardLayout("block_striped", n, g, lb)
+    mask = bb.block_sparse_mask(A["block_mask"], mb)
+    res = run_engine(layout, mask, A["q"], A["k"], A["v"], A["do"], bb.Topology(1, g), backward)
+    for h in range(hq):
+        assert np.max(np.abs(res["o"][:, h, :d] - A[f"o{h}"])) < 3e-2, h
+        assert np.max(np.abs(res["lse"][h] - A[f"lse{h}"])) < 1e-2, h
+        assert rel(res["dq"][:, h, :d], A[f"dq{h}"]) < 3e-2, h
+    assert rel(res["dk"][:, 0, :d], A["dk0"] + A["dk1"]) < 3e-2
+    assert rel(res["dv"][:, 0, :d], A["dv0"] + A["dv1"]) < 3e-2
+
+
 def test_reference_style_api_2d(cuda):
     """2-D [N, d] arrays in, reference-shaped NumPy out (forward_results / backward_grads)."""
     n, d, g = 64, 16, 4
